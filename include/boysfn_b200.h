@@ -1,0 +1,140 @@
+/*
+ * boysfn_b200.h -- C ABI of the B200-native batched Boys-function evaluator.
+ *
+ * This is the drop-in boundary for the reference hot path
+ *   void boysfn::boys_batch_many(std::span<const double> xs, int k,
+ *                                const boysfn::CoefficientTableSet& tables,
+ *                                std::span<double> out);
+ * (/root/reference/proj/core/include/boysfn/eval.hpp:43-45, implemented at
+ *  /root/reference/proj/core/src/eval.cpp:88-96).  The reference has no FFI of
+ * its own; this header is what a binding (cgo / JNI / ctypes / the C++ shim in
+ * paper_2512_10059_b200/cpp/) links against.  Plain C types only: no
+ * exceptions cross it, every entry point returns a boysfn_status, streams are
+ * passed as opaque cudaStream_t handles (void*; NULL = legacy default stream).
+ *
+ * Thread safety: table handles are immutable after creation and may be shared
+ * across threads and streams; concurrent calls on different streams are safe.
+ */
+#ifndef BOYSFN_B200_H
+#define BOYSFN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BOYSFN_ABI_VERSION 1
+
+/* Error convention.  The reference throws C++ exceptions; each maps to one code
+ * and the C++ shim rethrows the same type with the same message. */
+typedef enum boysfn_status {
+  BOYSFN_OK = 0,
+  BOYSFN_ERR_SIZE = 1,        /* std::invalid_argument, eval.cpp:90-91            */
+  BOYSFN_ERR_DOMAIN = 2,      /* std::domain_error, x < 0 or non-finite, eval.cpp:14-15 */
+  BOYSFN_ERR_RANGE = 3,       /* std::out_of_range, k outside [0, k_max], eval.cpp:16-17 */
+  BOYSFN_ERR_TABLES = 4,      /* std::invalid_argument from validate_tables, tables.cpp:14-32 */
+  BOYSFN_ERR_CUDA = 5,        /* a CUDA runtime error (no reference equivalent)   */
+  BOYSFN_ERR_ARG = 6,         /* NULL handle/pointer or bad layout/ld             */
+  BOYSFN_ERR_UNSUPPORTED = 7  /* k > 32 or a table degree beyond the device image */
+} boysfn_status;
+
+/* Output layout.  AOS is the reference's row-major out[i*(k+1)+l]
+ * (eval.cpp:94); SOA (out[l*ld+i]) is a north-star addition. */
+typedef enum boysfn_layout { BOYSFN_LAYOUT_AOS = 0, BOYSFN_LAYOUT_SOA = 1 } boysfn_layout;
+
+/* Region seam, boysfn::Region (eval.hpp:17). */
+typedef enum boysfn_region { BOYSFN_REGION_A = 0, BOYSFN_REGION_B = 1, BOYSFN_REGION_C = 2 } boysfn_region;
+
+/* Flattened boysfn::RationalApproximant (tables.hpp:12-17): ascending degree,
+ * numer has n+1 and denom m+1 entries, denom[m] == 1 (monic). */
+typedef struct boysfn_rational_desc {
+  int n;
+  int m;
+  const double* numer;
+  const double* denom;
+} boysfn_rational_desc;
+
+/* Flattened boysfn::CoefficientTableSet (tables.hpp:21-28). */
+typedef struct boysfn_table_desc {
+  double x0;
+  double x1;
+  int k_max;
+  double eps_tol;
+  boysfn_rational_desc r_B;
+  const boysfn_rational_desc* r_A; /* k_max + 1 entries, indexed by k */
+} boysfn_table_desc;
+
+/* Opaque immutable device-side table image built from a table set. */
+typedef struct boysfn_tables_s* boysfn_tables_t;
+
+/* Largest order the device kernels evaluate (templated unrolled chains). */
+#define BOYSFN_DEVICE_KMAX 32
+/* Largest numerator / denominator degree the device image holds. */
+#define BOYSFN_DEVICE_MAX_DEGREE 23
+
+int boysfn_abi_version(void);
+const char* boysfn_status_string(int status);
+/* Message of the last error on the calling thread (exact reference wording for
+ * SIZE/DOMAIN/RANGE/TABLES, CUDA error text for CUDA). */
+const char* boysfn_last_error(void);
+
+/* Build a table handle from a table set; validates like validate_tables
+ * (tables.cpp:14-32) and copies the coefficients.  Replaces passing
+ * `const CoefficientTableSet&` (eval.hpp:44) across the boundary. */
+int boysfn_tables_create(const boysfn_table_desc* desc, boysfn_tables_t* out);
+/* Process-lifetime handle of the embedded Appendix-C set (k_max = 32,
+ * eps = 5e-14), the device image of embedded_default() (tables_data.cpp:8). */
+int boysfn_tables_embedded(boysfn_tables_t* out);
+/* Destroying the embedded handle is a no-op. */
+int boysfn_tables_destroy(boysfn_tables_t tables);
+int boysfn_tables_info(boysfn_tables_t tables, double* x0, double* x1, int* k_max,
+                       double* eps_tol);
+
+/* Device entry point: x and out already resident in HBM.  Evaluates
+ * F_0..F_k for all n arguments, enqueued on `stream`, asynchronous.
+ *   layout AOS: out[i*(k+1)+l]  (ld ignored)
+ *   layout SOA: out[l*ld+i]     (ld >= n)
+ * Invalid x (negative, NaN, +-inf) does not stop the launch: when
+ * d_first_bad is non-NULL the kernel lowers *d_first_bad (a device uint64 the
+ * caller initialised, e.g. to UINT64_MAX) to the smallest offending index with
+ * atomicMin; rows at and after that index are unspecified.  Returns
+ * BOYSFN_ERR_RANGE for k outside [0, k_max] (host-side, nothing launched). */
+int boysfn_eval_device(boysfn_tables_t tables, const double* d_x, size_t n, int k,
+                       double* d_out, int layout, size_t ld, void* stream,
+                       unsigned long long* d_first_bad);
+
+/* Host entry point with boys_batch_many semantics (eval.cpp:88-96): xs and out
+ * are host buffers (pageable or pinned), out_len must equal n*(k+1) for AOS
+ * (else BOYSFN_ERR_SIZE) or ld*(k+1) with ld >= n for SOA.  Streams the batch
+ * through the device in chunks with host<->device copies overlapped with the
+ * kernels, and synchronises before returning.  On a bad x the rows before it
+ * are written, later rows are left untouched and *first_bad (if non-NULL)
+ * receives its index, exactly like the reference's first-throw behaviour. */
+int boysfn_eval_host(boysfn_tables_t tables, const double* xs, size_t n, int k, double* out,
+                     size_t out_len, int layout, size_t ld, size_t* first_bad);
+
+/* Forced-region evaluation of one x (boys_batch_region, eval.cpp:59-81, the
+ * reference's branch-agreement test seam), computed on the device. */
+int boysfn_eval_region_host(boysfn_tables_t tables, double x, int k, int region, double* out);
+
+/* Synthetic workload: x[i] = lo + (hi-lo)*u_i with u_i = (splitmix64(seed +
+ * (offset+i+1)*0x9E3779B97F4A7C15) >> 11) * 2^-53, the multiply and add
+ * separately rounded, so any CPU restating the formula reproduces it bit for
+ * bit and a shard [offset, offset+n) of the global stream is independent of
+ * the shard count. */
+int boysfn_generate_uniform(double* d_x, size_t n, uint64_t seed, uint64_t offset, double lo,
+                            double hi, void* stream);
+/* x[i] = 10^(log10_lo + (log10_hi-log10_lo)*u_i) (same u_i). */
+int boysfn_generate_loguniform(double* d_x, size_t n, uint64_t seed, uint64_t offset,
+                               double log10_lo, double log10_hi, void* stream);
+
+/* Number of this library's kernels launched by the calling process so far
+ * (bench.py reports the delta over its timed region as gpu_launches). */
+unsigned long long boysfn_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BOYSFN_B200_H */

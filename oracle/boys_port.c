@@ -1,0 +1,174 @@
+/*
+ * oracle/boys_port.c -- TEST INFRASTRUCTURE ONLY (the checker, never the product).
+ *
+ * A plain-C restatement of the reference hot path, Algorithm 1 of
+ * arXiv 2512.10059 as implemented in /root/reference/proj/core/src/eval.cpp.
+ * It performs the same double-precision operations in the same order as the
+ * reference so that, compiled with -O2 -ffp-contract=off (the reference is
+ * built -O2 without -march, hence without FMA: proj/CMakeLists.txt:6-8,
+ * core/CMakeLists.txt:32), it is bit-identical to the reference.  That claim is
+ * pinned by tests/test_oracle.py against the compiled reference (oracle/_ref)
+ * and against the committed golden vectors in tests/golden/.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * arm may load this file's library.  The CUDA product path never calls it.
+ */
+#include "boys_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* sqrt(pi)/2, correctly rounded -- eval.cpp:11 */
+static const double kHalfSqrtPiOracle = 0.88622692545275801364908374167057;
+
+/* check_input -- eval.cpp:13-18: x checked before k. */
+static int port_check_input(double x, int k, const oracle_tables* t) {
+  if (!isfinite(x) || x < 0) return ORACLE_ERR_DOMAIN;
+  if (k < 0 || k > t->k_max) return ORACLE_ERR_RANGE;
+  return ORACLE_OK;
+}
+
+/* classify_region -- eval.cpp:22-26 (half-open: boundary doubles go right). */
+int oracle_classify_region(double x, const oracle_tables* t) {
+  if (x < t->x0) return ORACLE_REGION_A;
+  if (x < t->x1) return ORACLE_REGION_B;
+  return ORACLE_REGION_C;
+}
+
+/* eval_rational -- eval.cpp:28-36: Horner from the top of ascending storage,
+ * separate multiply and add (no contraction), one division. */
+double oracle_eval_rational(const oracle_rational* r, double x) {
+  double num = r->numer[r->n];
+  for (int i = r->n; i-- > 0;) num = num * x + r->numer[i];
+  double den = r->denom[r->m];
+  for (int i = r->m; i-- > 0;) den = den * x + r->denom[i];
+  return num / den;
+}
+
+/* downward_recursion -- eval.cpp:38-47. */
+static void port_downward(double seed, double x, int k, double* out) {
+  out[k] = seed;
+  if (k == 0) return;
+  const double e = exp(-x);
+  const double twox = 2.0 * x;
+  for (int l = k - 1; l >= 0; --l) out[l] = (twox * out[l + 1] + e) / (2 * l + 1);
+}
+
+/* upward_recursion -- eval.cpp:49-57 (exp evaluated even for k == 0). */
+static void port_upward(double seed, double x, int k, double* out) {
+  out[0] = seed;
+  const double e = exp(-x);
+  const double twox = 2.0 * x;
+  for (int l = 0; l < k; ++l) out[l + 1] = ((2 * l + 1) * out[l] - e) / twox;
+}
+
+/* boys_batch_region -- eval.cpp:59-81 (region forced; test seam). */
+int oracle_boys_batch_region(double x, int k, const oracle_tables* t, int region,
+                             double* out) {
+  int st = port_check_input(x, k, t);
+  if (st != ORACLE_OK) return st;
+  switch (region) {
+    case ORACLE_REGION_A:
+      port_downward(oracle_eval_rational(&t->r_A[k], x), x, k, out);
+      break;
+    case ORACLE_REGION_B:
+      if (!(x > 0)) return ORACLE_ERR_DOMAIN; /* upward_recursion precondition, eval.cpp:50 */
+      port_upward(oracle_eval_rational(&t->r_B, x), x, k, out);
+      break;
+    default: {
+      out[0] = kHalfSqrtPiOracle / sqrt(x);
+      const double inv2x = 0.5 / x;
+      for (int l = 0; l < k; ++l) out[l + 1] = (2 * l + 1) * inv2x * out[l];
+      break;
+    }
+  }
+  return ORACLE_OK;
+}
+
+/* boys_batch -- eval.cpp:83-86. */
+int oracle_boys_batch(double x, int k, const oracle_tables* t, double* out) {
+  int st = port_check_input(x, k, t);
+  if (st != ORACLE_OK) return st;
+  return oracle_boys_batch_region(x, k, t, oracle_classify_region(x, t), out);
+}
+
+/* boys_batch_many -- eval.cpp:88-96.  Rows before the first bad x are written,
+ * later rows are untouched; *first_bad receives the offending index. */
+int oracle_boys_batch_many(const double* xs, size_t n, int k, const oracle_tables* t,
+                           double* out, size_t out_len, size_t* first_bad) {
+  if (out_len != n * ((size_t)k + 1)) return ORACLE_ERR_SIZE;
+  const size_t row = (size_t)k + 1;
+  for (size_t i = 0; i < n; ++i) {
+    int st = oracle_boys_batch(xs[i], k, t, out + i * row);
+    if (st != ORACLE_OK) {
+      if (first_bad) *first_bad = i;
+      return st;
+    }
+  }
+  return ORACLE_OK;
+}
+
+/* ---- multi-threaded driver for the CPU baseline (disjoint spans; the path is
+ * reentrant).  Threads are the only addition to the reference. */
+typedef struct {
+  const double* xs;
+  size_t n;
+  int k;
+  const oracle_tables* t;
+  double* out;
+  int status;
+  size_t bad;
+} port_job;
+
+static void* port_worker(void* arg) {
+  port_job* j = (port_job*)arg;
+  j->status = oracle_boys_batch_many(j->xs, j->n, j->k, j->t, j->out,
+                                     j->n * ((size_t)j->k + 1), &j->bad);
+  return NULL;
+}
+
+int oracle_boys_batch_many_mt(const double* xs, size_t n, int k, const oracle_tables* t,
+                              double* out, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if ((size_t)nthreads > n) nthreads = n ? (int)n : 1;
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  port_job* jobs = (port_job*)calloc((size_t)nthreads, sizeof(port_job));
+  const size_t row = (size_t)k + 1;
+  size_t begin = 0;
+  for (int w = 0; w < nthreads; ++w) {
+    size_t cnt = n / nthreads + ((size_t)w < n % nthreads ? 1 : 0);
+    jobs[w] = (port_job){xs + begin, cnt, k, t, out + begin * row, 0, 0};
+    pthread_create(&th[w], NULL, port_worker, &jobs[w]);
+    begin += cnt;
+  }
+  int st = ORACLE_OK;
+  for (int w = 0; w < nthreads; ++w) {
+    pthread_join(th[w], NULL);
+    if (st == ORACLE_OK && jobs[w].status != ORACLE_OK) st = jobs[w].status;
+  }
+  free(th);
+  free(jobs);
+  return st;
+}
+
+/* ---- synthetic workload generator shared with the device generator
+ * (paper_2512_10059_b200/csrc/boys_kernels.cu: gen_uniform_kernel).  splitmix64
+ * keyed by the global index, so shards of any size reproduce one stream. */
+static uint64_t splitmix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+void oracle_gen_uniform(double* x, size_t n, uint64_t seed, uint64_t offset, double lo,
+                        double hi) {
+  const double span = hi - lo;
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t z = splitmix64(seed + (offset + i + 1) * 0x9E3779B97F4A7C15ULL);
+    const double u = (double)(z >> 11) * 0x1.0p-53;
+    x[i] = lo + span * u; /* -ffp-contract=off: mul and add rounded separately */
+  }
+}

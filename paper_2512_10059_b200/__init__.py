@@ -1,0 +1,21 @@
+"""B200-native batched Boys-function evaluator (arXiv 2512.10059, Algorithm 1).
+
+Drop-in for the reference's evaluation API (boysfn::boys_batch_many & co.,
+/root/reference/proj/core/include/boysfn/eval.hpp): the C ABI is
+include/boysfn_b200.h, the C++ shim paper_2512_10059_b200/cpp/, and this
+package is the Python mirror.  All evaluation runs in hand-written sm_100a
+FP64 kernels (csrc/); see DESIGN.md.
+"""
+from .tables import (CoefficientTableSet, RationalApproximant, TableParseError, embedded_default,
+                     emit_tables, parse_tables, validate_tables)
+from .eval import (BoysBatch, DeviceTables, Region, boys_batch, boys_batch_many, boys_batch_region,
+                   classify_region, cuda_error, domain_error, eval_device, generate_loguniform,
+                   generate_uniform, invalid_argument, kernel_launch_count, out_of_range, unsupported)
+
+__all__ = [
+    "CoefficientTableSet", "RationalApproximant", "TableParseError", "embedded_default", "emit_tables",
+    "parse_tables", "validate_tables", "BoysBatch", "DeviceTables", "Region", "boys_batch",
+    "boys_batch_many", "boys_batch_region", "classify_region", "cuda_error", "domain_error",
+    "eval_device", "generate_loguniform", "generate_uniform", "invalid_argument",
+    "kernel_launch_count", "out_of_range", "unsupported",
+]

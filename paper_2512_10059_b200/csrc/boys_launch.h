@@ -1,0 +1,27 @@
+// boys_launch.h -- host-side internals shared by the kernel instantiation units
+// and the C ABI (capi.cu).  Not installed; the public surface is
+// include/boysfn_b200.h.
+#pragma once
+
+#include "boys_device.cuh"
+
+namespace boysfn_dev {
+
+// Degree variants of the kernel for one order k.
+//   kVariantEmbedded: the exact (n, m) of the paper's tables for that k
+//                     (r_A[k] per Appendix C, r_B = (5, 6)); used whenever a
+//                     table set has that degree profile.
+//   kVariantPadded:   every rational padded to kMaxCoef-1 (any custom set).
+enum Variant : int { kVariantEmbedded = 0, kVariantPadded = 1 };
+
+constexpr int kKernelKmax = 32;
+
+// Kernel entry points, one translation unit per store path.
+const void* kernel_soa(int k, int variant);
+const void* kernel_aos_tma(int k, int variant);
+const void* kernel_aos_xpose(int k, int variant);
+
+// Exact degrees of the embedded kernels (from embedded_tables.inc).
+void embedded_degrees(int k, int* na, int* ma, int* nb, int* mb);
+
+}  // namespace boysfn_dev

@@ -1,0 +1,493 @@
+// capi.cu -- the C ABI of include/boysfn_b200.h: table handles, kernel
+// dispatch, the chunked host<->device pipeline behind boys_batch_many, and the
+// synthetic-workload generators.  Every evaluation runs on the GPU; there is no
+// CPU fallback: without a device the calls return BOYSFN_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/boysfn_b200.h"
+#include "boys_launch.h"
+#include "embedded_tables.inc"
+
+#define BOYSFN_API extern "C" __attribute__((visibility("default")))
+
+using boysfn_dev::EvalParams;
+using boysfn_dev::kMaxCoef;
+
+// ----------------------------------------------------------------- errors --
+namespace {
+
+// Exact reference wording (eval.cpp:14-17,51,90-91; tables.cpp:15-28).
+constexpr const char* kMsgSize = "boys_batch_many: output span has wrong size";
+constexpr const char* kMsgDomain = "boys_batch: x must be finite and non-negative";
+constexpr const char* kMsgRange = "boys_batch: k out of range for this table set";
+constexpr const char* kMsgUpward = "upward_recursion: x must be positive";
+
+thread_local std::string t_last_error;
+
+int fail(int status, const std::string& msg) {
+  t_last_error = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  t_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return BOYSFN_ERR_CUDA;
+}
+
+#define CUDA_TRY(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+std::atomic<unsigned long long> g_launches{0};
+
+}  // namespace
+
+// ------------------------------------------------------------ table image --
+struct boysfn_tables_s {
+  double x0 = 0, x1 = 0, eps_tol = 0;
+  int k_max = 0;
+  bool is_embedded = false;
+  std::vector<EvalParams> params;  // one launch image per order k <= device kmax
+  std::vector<int> variant;        // kernel degree variant per k
+  std::vector<int> degree_ok;      // 1 if r_A[k], r_B fit the device image
+};
+
+namespace {
+
+bool fill_rational(const boysfn_rational_desc& r, double* num, double* den) {
+  if (r.n > kMaxCoef - 1 || r.m > kMaxCoef - 1) return false;
+  std::fill(num, num + kMaxCoef, 0.0);
+  std::fill(den, den + kMaxCoef, 0.0);
+  std::copy(r.numer, r.numer + r.n + 1, num);
+  std::copy(r.denom, r.denom + r.m + 1, den);
+  return true;
+}
+
+// validate_tables (tables.cpp:14-32), same order and messages.
+int validate_desc(const boysfn_table_desc* d) {
+  if (d->k_max < 0) return fail(BOYSFN_ERR_TABLES, "tables: k_max must be non-negative");
+  if (!(d->eps_tol > 0)) return fail(BOYSFN_ERR_TABLES, "tables: eps_tol must be positive");
+  if (!(d->x0 > 0 && d->x0 < d->x1)) return fail(BOYSFN_ERR_TABLES, "tables: need 0 < x0 < x1");
+  if (d->r_A == nullptr)
+    return fail(BOYSFN_ERR_TABLES, "tables: need exactly k_max+1 region-A tables");
+  auto check = [](const boysfn_rational_desc& r, const std::string& what) -> int {
+    if (r.n < 0 || r.m < 0 || r.numer == nullptr || r.denom == nullptr)
+      return fail(BOYSFN_ERR_TABLES, "tables: empty coefficient vector in " + what);
+    for (int i = 0; i <= r.n; ++i)
+      if (!std::isfinite(r.numer[i])) return fail(BOYSFN_ERR_TABLES, "tables: non-finite value in " + what);
+    for (int i = 0; i <= r.m; ++i)
+      if (!std::isfinite(r.denom[i])) return fail(BOYSFN_ERR_TABLES, "tables: non-finite value in " + what);
+    if (r.denom[r.m] != 1.0)
+      return fail(BOYSFN_ERR_TABLES, "tables: non-monic denominator in " + what);
+    return BOYSFN_OK;
+  };
+  if (int st = check(d->r_B, "r_B")) return st;
+  for (int k = 0; k <= d->k_max; ++k)
+    if (int st = check(d->r_A[k], "r_A[" + std::to_string(k) + "]")) return st;
+  return BOYSFN_OK;
+}
+
+int build_handle(const boysfn_table_desc* d, boysfn_tables_s* h) {
+  h->x0 = d->x0;
+  h->x1 = d->x1;
+  h->eps_tol = d->eps_tol;
+  h->k_max = d->k_max;
+  const int kdev = std::min(d->k_max, boysfn_dev::kKernelKmax);
+  h->params.assign(kdev + 1, EvalParams{});
+  h->variant.assign(kdev + 1, boysfn_dev::kVariantPadded);
+  h->degree_ok.assign(kdev + 1, 0);
+  for (int k = 0; k <= kdev; ++k) {
+    EvalParams& p = h->params[k];
+    p.x0 = d->x0;
+    p.x1 = d->x1;
+    p.force_region = -1;
+    const bool ok = fill_rational(d->r_A[k], p.numA, p.denA) && fill_rational(d->r_B, p.numB, p.denB);
+    h->degree_ok[k] = ok ? 1 : 0;
+    int na, ma, nb, mb;
+    boysfn_dev::embedded_degrees(k, &na, &ma, &nb, &mb);
+    if (d->r_A[k].n == na && d->r_A[k].m == ma && d->r_B.n == nb && d->r_B.m == mb)
+      h->variant[k] = boysfn_dev::kVariantEmbedded;
+  }
+  return BOYSFN_OK;
+}
+
+boysfn_tables_s* embedded_handle() {
+  static boysfn_tables_s* h = [] {
+    std::vector<boysfn_rational_desc> ra(BOYSFN_EMB_KMAX + 1);
+    for (int k = 0; k <= BOYSFN_EMB_KMAX; ++k)
+      ra[k] = boysfn_rational_desc{kEmbDegA[k][0], kEmbDegA[k][1], kEmbNumA[k], kEmbDenA[k]};
+    boysfn_table_desc d{BOYSFN_EMB_X0, BOYSFN_EMB_X1, BOYSFN_EMB_KMAX, BOYSFN_EMB_EPS,
+                        boysfn_rational_desc{kEmbDegB[0], kEmbDegB[1], kEmbNumB, kEmbDenB},
+                        ra.data()};
+    auto* t = new boysfn_tables_s;
+    build_handle(&d, t);
+    t->is_embedded = true;
+    return t;
+  }();
+  return h;
+}
+
+// ------------------------------------------------------------- dispatch --
+struct DeviceInfo {
+  int sms = 0;
+  std::map<const void*, int> blocks_per_sm;
+};
+
+std::mutex g_dev_mu;
+std::map<int, DeviceInfo> g_devices;
+
+int occupancy(const void* fn, size_t smem, int* sms, int* bps) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  DeviceInfo& di = g_devices[dev];
+  if (di.sms == 0) CUDA_TRY(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+  auto it = di.blocks_per_sm.find(fn);
+  if (it == di.blocks_per_sm.end()) {
+    int b = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, boysfn_dev::kThreadsPerBlock, smem));
+    it = di.blocks_per_sm.emplace(fn, std::max(b, 1)).first;
+  }
+  *sms = di.sms;
+  *bps = it->second;
+  return BOYSFN_OK;
+}
+
+bool force_xpose() {
+  static const bool v = [] {
+    const char* e = std::getenv("BOYSFN_AOS_PATH");
+    return e != nullptr && std::strcmp(e, "xpose") == 0;
+  }();
+  return v;
+}
+
+// Launches the evaluation kernel; k already validated against the handle.
+int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out,
+                int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad,
+                int force_region) {
+  if (n == 0) return BOYSFN_OK;
+  if (k > boysfn_dev::kKernelKmax)
+    return fail(BOYSFN_ERR_UNSUPPORTED, "device kernels evaluate k <= 32");
+  if (!t->degree_ok[k])
+    return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
+  const int R = k + 1;
+  const void* fn = nullptr;
+  size_t smem = 0;
+  if (layout == BOYSFN_LAYOUT_SOA) {
+    fn = boysfn_dev::kernel_soa(k, t->variant[k]);
+  } else if ((R & 1) && (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && !force_xpose()) {
+    fn = boysfn_dev::kernel_aos_tma(k, t->variant[k]);
+    smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * 32 * R;
+  } else {
+    fn = boysfn_dev::kernel_aos_xpose(k, t->variant[k]);
+    smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::kXposePitch * R;
+  }
+  int sms = 0, bps = 0;
+  if (int st = occupancy(fn, smem, &sms, &bps)) return st;
+  const size_t ntiles = (n + 31) / 32;
+  const size_t want = (ntiles + boysfn_dev::kWarpsPerBlock - 1) / boysfn_dev::kWarpsPerBlock;
+  const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
+  EvalParams p = t->params[k];
+  p.force_region = force_region;
+  void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad};
+  CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, smem, stream));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BOYSFN_OK;
+}
+
+// --------------------------------------------------------- host pipeline --
+// Per (thread, device) staging: three slots, each with its own stream, so the
+// H2D copy + kernel of chunk c+2 and the D2H copy of chunk c overlap.
+struct Pipeline {
+  static constexpr int kSlots = 3;
+  static constexpr size_t kChunkOutBytes = size_t(128) << 20;
+  int device = -1;
+  cudaStream_t stream[kSlots] = {};
+  cudaEvent_t done[kSlots] = {};
+  double* d_x[kSlots] = {};
+  double* d_out[kSlots] = {};
+  unsigned long long* d_bad = nullptr;  // kSlots words
+  unsigned long long* h_bad = nullptr;  // pinned, kSlots words
+  size_t cap_x = 0;                     // x capacity per slot
+  size_t cap_out = 0;                   // doubles per slot
+
+  int init(int dev) {
+    device = dev;
+    for (int s = 0; s < kSlots; ++s) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&stream[s], cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaMalloc(&d_bad, kSlots * sizeof(unsigned long long)));
+    CUDA_TRY(cudaHostAlloc(&h_bad, kSlots * sizeof(unsigned long long), cudaHostAllocDefault));
+    cap_out = kChunkOutBytes / sizeof(double);
+    cap_x = cap_out;  // enough for k = 0
+    for (int s = 0; s < kSlots; ++s) {
+      CUDA_TRY(cudaMalloc(&d_x[s], cap_x * sizeof(double)));
+      CUDA_TRY(cudaMalloc(&d_out[s], cap_out * sizeof(double)));
+    }
+    return BOYSFN_OK;
+  }
+};
+
+int get_pipeline(Pipeline** out) {
+  thread_local std::map<int, std::unique_ptr<Pipeline>> pipes;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  auto& p = pipes[dev];
+  if (!p) {
+    auto np = std::make_unique<Pipeline>();
+    if (int st = np->init(dev)) return st;
+    p = std::move(np);
+  }
+  *out = p.get();
+  return BOYSFN_OK;
+}
+
+bool x_ok(double x) { return std::isfinite(x) && x >= 0; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI --
+BOYSFN_API int boysfn_abi_version(void) { return BOYSFN_ABI_VERSION; }
+
+BOYSFN_API const char* boysfn_status_string(int status) {
+  switch (status) {
+    case BOYSFN_OK: return "ok";
+    case BOYSFN_ERR_SIZE: return "invalid_argument: output size mismatch";
+    case BOYSFN_ERR_DOMAIN: return "domain_error: x must be finite and non-negative";
+    case BOYSFN_ERR_RANGE: return "out_of_range: k outside [0, k_max]";
+    case BOYSFN_ERR_TABLES: return "invalid_argument: invalid coefficient table set";
+    case BOYSFN_ERR_CUDA: return "CUDA error";
+    case BOYSFN_ERR_ARG: return "invalid argument";
+    case BOYSFN_ERR_UNSUPPORTED: return "unsupported by the device kernels";
+    default: return "unknown status";
+  }
+}
+
+BOYSFN_API const char* boysfn_last_error(void) { return t_last_error.c_str(); }
+
+BOYSFN_API int boysfn_tables_create(const boysfn_table_desc* desc, boysfn_tables_t* out) {
+  if (desc == nullptr || out == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
+  if (int st = validate_desc(desc)) return st;
+  auto* h = new boysfn_tables_s;
+  build_handle(desc, h);
+  *out = h;
+  return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_tables_embedded(boysfn_tables_t* out) {
+  if (out == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
+  *out = embedded_handle();
+  return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_tables_destroy(boysfn_tables_t t) {
+  if (t != nullptr && !t->is_embedded) delete t;
+  return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_tables_info(boysfn_tables_t t, double* x0, double* x1, int* k_max,
+                                  double* eps_tol) {
+  if (t == nullptr) return fail(BOYSFN_ERR_ARG, "null handle");
+  if (x0) *x0 = t->x0;
+  if (x1) *x1 = t->x1;
+  if (k_max) *k_max = t->k_max;
+  if (eps_tol) *eps_tol = t->eps_tol;
+  return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_eval_device(boysfn_tables_t t, const double* d_x, size_t n, int k,
+                                  double* d_out, int layout, size_t ld, void* stream,
+                                  unsigned long long* d_first_bad) {
+  if (t == nullptr) return fail(BOYSFN_ERR_ARG, "null handle");
+  if (k < 0 || k > t->k_max) return fail(BOYSFN_ERR_RANGE, kMsgRange);
+  if (layout != BOYSFN_LAYOUT_AOS && layout != BOYSFN_LAYOUT_SOA)
+    return fail(BOYSFN_ERR_ARG, "layout must be AOS or SOA");
+  if (n == 0) return BOYSFN_OK;
+  if (d_x == nullptr || d_out == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
+  if (layout == BOYSFN_LAYOUT_SOA && ld < n) return fail(BOYSFN_ERR_ARG, "SOA ld must be >= n");
+  return launch_eval(t, d_x, n, k, d_out, layout, ld, static_cast<cudaStream_t>(stream),
+                     d_first_bad, -1);
+}
+
+BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, int k, double* out,
+                                size_t out_len, int layout, size_t ld, size_t* first_bad) {
+  if (t == nullptr) return fail(BOYSFN_ERR_ARG, "null handle");
+  if (layout != BOYSFN_LAYOUT_AOS && layout != BOYSFN_LAYOUT_SOA)
+    return fail(BOYSFN_ERR_ARG, "layout must be AOS or SOA");
+  // eval.cpp:90-91: size check first (k+1 computed in size_t, as the reference).
+  const size_t row = static_cast<size_t>(k) + 1;
+  if (layout == BOYSFN_LAYOUT_AOS) {
+    if (out_len != n * row) return fail(BOYSFN_ERR_SIZE, kMsgSize);
+    ld = n;
+  } else {
+    if (ld < n) return fail(BOYSFN_ERR_ARG, "SOA ld must be >= n");
+    if (out_len != ld * row) return fail(BOYSFN_ERR_SIZE, kMsgSize);
+  }
+  if (n == 0) return BOYSFN_OK;
+  if (xs == nullptr || out == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
+  // check_input (eval.cpp:13-18) at the first row: x before k.
+  if (k < 0 || k > t->k_max) {
+    if (first_bad) *first_bad = 0;
+    return x_ok(xs[0]) ? fail(BOYSFN_ERR_RANGE, kMsgRange) : fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
+  }
+  Pipeline* P = nullptr;
+  if (int st = get_pipeline(&P)) return st;
+  const size_t cx = std::max<size_t>(32, std::min(P->cap_x, P->cap_out / row) / 32 * 32);
+  const size_t nchunks = (n + cx - 1) / cx;
+  const int S = Pipeline::kSlots;
+
+  auto issue = [&](size_t c) -> int {
+    const int s = static_cast<int>(c % S);
+    const size_t off = c * cx, cn = std::min(cx, n - off);
+    CUDA_TRY(cudaMemcpyAsync(P->d_x[s], xs + off, cn * sizeof(double), cudaMemcpyHostToDevice, P->stream[s]));
+    CUDA_TRY(cudaMemsetAsync(P->d_bad + s, 0xFF, sizeof(unsigned long long), P->stream[s]));
+    if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], P->d_bad + s, -1))
+      return st;
+    CUDA_TRY(cudaMemcpyAsync(P->h_bad + s, P->d_bad + s, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             P->stream[s]));
+    CUDA_TRY(cudaEventRecord(P->done[s], P->stream[s]));
+    return BOYSFN_OK;
+  };
+  auto drain = [&]() {
+    for (int s = 0; s < S; ++s) cudaStreamSynchronize(P->stream[s]);
+  };
+
+  int status = BOYSFN_OK;
+  for (size_t c = 0; c < std::min<size_t>(nchunks, S - 1); ++c)
+    if ((status = issue(c))) break;
+  for (size_t c = 0; c < nchunks && status == BOYSFN_OK; ++c) {
+    if (c + S - 1 < nchunks && (status = issue(c + S - 1))) break;
+    const int s = static_cast<int>(c % S);
+    const size_t off = c * cx, cn = std::min(cx, n - off);
+    if (cudaError_t e = cudaEventSynchronize(P->done[s])) {
+      status = cuda_fail(e, "cudaEventSynchronize");
+      break;
+    }
+    const unsigned long long bad = P->h_bad[s];
+    const size_t rows = bad == ~0ull ? cn : static_cast<size_t>(bad);
+    if (rows > 0) {
+      cudaError_t e;
+      if (layout == BOYSFN_LAYOUT_AOS)
+        e = cudaMemcpyAsync(out + off * row, P->d_out[s], rows * row * sizeof(double),
+                            cudaMemcpyDeviceToHost, P->stream[s]);
+      else
+        e = cudaMemcpy2DAsync(out + off, ld * sizeof(double), P->d_out[s], cn * sizeof(double),
+                              rows * sizeof(double), row, cudaMemcpyDeviceToHost, P->stream[s]);
+      if (e != cudaSuccess) {
+        status = cuda_fail(e, "cudaMemcpyAsync D2H");
+        break;
+      }
+    }
+    if (bad != ~0ull) {
+      if (first_bad) *first_bad = off + static_cast<size_t>(bad);
+      status = fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
+    }
+  }
+  drain();
+  if (status == BOYSFN_OK) {
+    if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "boysfn_eval_host");
+  }
+  return status;
+}
+
+BOYSFN_API int boysfn_eval_region_host(boysfn_tables_t t, double x, int k, int region, double* out) {
+  if (t == nullptr || out == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
+  if (region < 0 || region > 2) return fail(BOYSFN_ERR_ARG, "region must be A, B or C");
+  if (!x_ok(x)) return fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
+  if (k < 0 || k > t->k_max) return fail(BOYSFN_ERR_RANGE, kMsgRange);
+  if (region == BOYSFN_REGION_B && !(x > 0)) return fail(BOYSFN_ERR_DOMAIN, kMsgUpward);
+  Pipeline* P = nullptr;
+  if (int st = get_pipeline(&P)) return st;
+  cudaStream_t s = P->stream[0];
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaMemcpyAsync(P->d_x[0], &x, sizeof(double), cudaMemcpyHostToDevice, s));
+  if (int st = launch_eval(t, P->d_x[0], 1, k, P->d_out[0], BOYSFN_LAYOUT_AOS, 1, s, nullptr, region))
+    return st;
+  CUDA_TRY(cudaMemcpyAsync(out, P->d_out[0], (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return BOYSFN_OK;
+}
+
+// -------------------------------------------------------- workload gens --
+namespace {
+
+__device__ __forceinline__ double uniform01(uint64_t seed, uint64_t idx) {
+  uint64_t z = seed + (idx + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return static_cast<double>(z >> 11) * 0x1.0p-53;
+}
+
+__global__ void gen_uniform_kernel(double* x, size_t n, uint64_t seed, uint64_t offset, double lo,
+                                   double span) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    x[i] = __dadd_rn(lo, __dmul_rn(span, uniform01(seed, offset + i)));
+}
+
+__global__ void gen_loguniform_kernel(double* x, size_t n, uint64_t seed, uint64_t offset, double lo,
+                                      double span) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    x[i] = exp10(__dadd_rn(lo, __dmul_rn(span, uniform01(seed, offset + i))));
+}
+
+int gen_grid(size_t n, unsigned* grid) {
+  int dev = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  *grid = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((n + 255) / 256, size_t(sms) * 8)));
+  return BOYSFN_OK;
+}
+
+}  // namespace
+
+BOYSFN_API int boysfn_generate_uniform(double* d_x, size_t n, uint64_t seed, uint64_t offset,
+                                       double lo, double hi, void* stream) {
+  if (n == 0) return BOYSFN_OK;
+  if (d_x == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
+  unsigned grid = 0;
+  if (int st = gen_grid(n, &grid)) return st;
+  gen_uniform_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_x, n, seed, offset, lo, hi - lo);
+  CUDA_TRY(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_generate_loguniform(double* d_x, size_t n, uint64_t seed, uint64_t offset,
+                                          double log10_lo, double log10_hi, void* stream) {
+  if (n == 0) return BOYSFN_OK;
+  if (d_x == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
+  unsigned grid = 0;
+  if (int st = gen_grid(n, &grid)) return st;
+  gen_loguniform_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_x, n, seed, offset, log10_lo,
+                                                                             log10_hi - log10_lo);
+  CUDA_TRY(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BOYSFN_OK;
+}
+
+BOYSFN_API unsigned long long boysfn_kernel_launch_count(void) {
+  return g_launches.load(std::memory_order_relaxed);
+}
+
+// Exact degrees of the embedded kernels (boys_launch.h).
+void boysfn_dev::embedded_degrees(int k, int* na, int* ma, int* nb, int* mb) {
+  *na = (k >= 0 && k <= BOYSFN_EMB_KMAX) ? kEmbDegA[k][0] : -1;
+  *ma = (k >= 0 && k <= BOYSFN_EMB_KMAX) ? kEmbDegA[k][1] : -1;
+  *nb = kEmbDegB[0];
+  *mb = kEmbDegB[1];
+}

@@ -1,0 +1,210 @@
+"""Evaluation API, Python mirror of the reference's eval.hpp, on the GPU.
+
+Same names and semantics as /root/reference/proj/core/include/boysfn/eval.hpp:
+  boys_batch_many(xs, k, tables, out)   eval.hpp:43-45 / eval.cpp:88-96
+  boys_batch(x, k, tables)              eval.hpp:37    / eval.cpp:83-86
+  boys_batch_region(x, k, tables, r)    eval.hpp:39-41 / eval.cpp:59-81
+  classify_region(x, tables)            eval.hpp:23    / eval.cpp:22-26
+Exceptions mirror the reference's C++ types (invalid_argument, domain_error,
+out_of_range) with its messages; rows before the first bad x are written and
+later rows untouched.  Every value is computed by the sm_100a kernels of
+libboysfn_b200.so through the C ABI (include/boysfn_b200.h); there is no CPU
+fallback.  `eval_device` is the HBM-resident entry point (torch CUDA tensors).
+"""
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+
+from . import _capi
+from .tables import CoefficientTableSet, embedded_default, validate_tables
+
+
+class invalid_argument(ValueError):
+    """std::invalid_argument."""
+
+
+class domain_error(ValueError):
+    """std::domain_error."""
+
+
+class out_of_range(IndexError):
+    """std::out_of_range."""
+
+
+class cuda_error(RuntimeError):
+    """A CUDA runtime failure (no reference equivalent)."""
+
+
+class unsupported(RuntimeError):
+    """k > 32 or a table degree the device image cannot hold."""
+
+
+def _raise(status, first_bad=None):
+    if status == _capi.OK:
+        return
+    msg = _capi.last_error()
+    exc = {
+        _capi.ERR_SIZE: invalid_argument,
+        _capi.ERR_DOMAIN: domain_error,
+        _capi.ERR_RANGE: out_of_range,
+        _capi.ERR_TABLES: invalid_argument,
+        _capi.ERR_CUDA: cuda_error,
+        _capi.ERR_ARG: invalid_argument,
+        _capi.ERR_UNSUPPORTED: unsupported,
+    }.get(status, RuntimeError)(msg)
+    if first_bad is not None:
+        exc.first_bad = first_bad
+    raise exc
+
+
+class Region(enum.IntEnum):
+    """eval.hpp:17."""
+    A = 0
+    B = 1
+    C = 2
+
+
+@dataclass
+class BoysBatch:
+    """eval.hpp:11-15."""
+    x: float = 0.0
+    k: int = 0
+    values: List[float] = field(default_factory=list)
+
+
+class DeviceTables:
+    """Device table handle for a CoefficientTableSet (boysfn_tables_t)."""
+
+    def __init__(self, tables):
+        L = _capi.lib()
+        self._h = ctypes.c_void_p()
+        self._owned = tables is not embedded_default()
+        if not self._owned:
+            _raise(L.boysfn_tables_embedded(ctypes.byref(self._h)))
+            return
+        validate_tables(tables)
+        keep = []
+
+        def desc(r):
+            nu = np.ascontiguousarray(r.numer, dtype=np.float64)
+            de = np.ascontiguousarray(r.denom, dtype=np.float64)
+            keep.extend((nu, de))
+            return _capi.RationalDesc(len(nu) - 1, len(de) - 1,
+                                      nu.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                      de.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        ra = (_capi.RationalDesc * len(tables.r_A))(*[desc(r) for r in tables.r_A])
+        d = _capi.TableDesc(tables.x0, tables.x1, tables.k_max, tables.eps_tol, desc(tables.r_B), ra)
+        _raise(L.boysfn_tables_create(ctypes.byref(d), ctypes.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h and self._owned:
+            _capi.lib().boysfn_tables_destroy(self._h)
+        self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_EMB_HANDLE = None
+
+
+def _handle(tables):
+    global _EMB_HANDLE
+    if tables is embedded_default():
+        if _EMB_HANDLE is None:
+            _EMB_HANDLE = DeviceTables(tables)
+        return _EMB_HANDLE
+    return DeviceTables(tables)
+
+
+def classify_region(x, tables):
+    """Half-open [0,x0)->A, [x0,x1)->B, [x1,inf)->C (eval.cpp:22-26)."""
+    if x < tables.x0:
+        return Region.A
+    if x < tables.x1:
+        return Region.B
+    return Region.C
+
+
+def boys_batch_many(xs, k, tables, out, layout="aos", ld=None):
+    """Host-buffer bulk entry (eval.cpp:88-96).  xs: float64 array of N x;
+    out: writable float64 array of N*(k+1) (AoS, row i = F_0..F_k(x_i)) or,
+    with layout="soa", ld*(k+1) doubles laid out out[l*ld+i]."""
+    L = _capi.lib()
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous):
+        raise invalid_argument("out must be a C-contiguous float64 numpy array")
+    lay = _capi.LAYOUT_SOA if layout == "soa" else _capi.LAYOUT_AOS
+    h = _handle(tables)
+    bad = ctypes.c_size_t(0)
+    st = L.boysfn_eval_host(h.handle, xs.ctypes.data, xs.size, int(k), out.ctypes.data, out.size, lay,
+                            int(ld if ld is not None else xs.size), ctypes.byref(bad))
+    _raise(st, bad.value if st == _capi.ERR_DOMAIN else None)
+
+
+def boys_batch(x, k, tables):
+    """One argument (eval.cpp:83-86)."""
+    out = np.empty(max(int(k) + 1, 0), dtype=np.float64)
+    if k < 0 or k > tables.k_max:
+        # same order of checks as check_input: x first, then k
+        boys_batch_many(np.array([x], dtype=np.float64), k, tables,
+                        np.empty(int(k) + 1 if k >= 0 else 0, dtype=np.float64))
+    boys_batch_many(np.array([x], dtype=np.float64), k, tables, out)
+    return BoysBatch(float(x), int(k), out.tolist())
+
+
+def boys_batch_region(x, k, tables, region):
+    """Forced region (eval.cpp:59-81), evaluated by the device kernel."""
+    L = _capi.lib()
+    out = np.empty(max(int(k) + 1, 1), dtype=np.float64)
+    h = _handle(tables)
+    _raise(L.boysfn_eval_region_host(h.handle, float(x), int(k), int(region), out.ctypes.data))
+    return BoysBatch(float(x), int(k), out[: int(k) + 1].tolist())
+
+
+def eval_device(x, k, out, tables=None, layout="soa", ld=None, stream=None, first_bad=None):
+    """HBM-resident entry point: x a CUDA float64 tensor of N arguments, out a
+    CUDA float64 tensor ((k+1)*ld for SoA, N*(k+1) for AoS).  Enqueued on
+    `stream` (default: torch's current stream), asynchronous.  first_bad: an
+    optional CUDA int64 tensor lowered to the smallest invalid index."""
+    import torch
+    L = _capi.lib()
+    tables = tables if tables is not None else embedded_default()
+    h = _handle(tables)
+    n = x.numel()
+    lay = _capi.LAYOUT_SOA if layout == "soa" else _capi.LAYOUT_AOS
+    ld = n if ld is None else int(ld)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    st = L.boysfn_eval_device(h.handle, x.data_ptr(), n, int(k), out.data_ptr(), lay, ld,
+                              ctypes.c_void_p(s.cuda_stream),
+                              first_bad.data_ptr() if first_bad is not None else None)
+    _raise(st)
+
+
+def generate_uniform(x, seed, lo, hi, offset=0, stream=None):
+    """Fill CUDA tensor x with the splitmix64 uniform stream (boysfn_b200.h)."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _raise(_capi.lib().boysfn_generate_uniform(x.data_ptr(), x.numel(), seed, offset, lo, hi,
+                                               ctypes.c_void_p(s.cuda_stream)))
+
+
+def generate_loguniform(x, seed, log10_lo, log10_hi, offset=0, stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _raise(_capi.lib().boysfn_generate_loguniform(x.data_ptr(), x.numel(), seed, offset, log10_lo,
+                                                  log10_hi, ctypes.c_void_p(s.cuda_stream)))
+
+
+def kernel_launch_count():
+    return int(_capi.lib().boysfn_kernel_launch_count())

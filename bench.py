@@ -1,0 +1,355 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 Boys-function evaluator (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+F_0..F_32 for 1e8 uniform x in [0,100] per GPU, SoA output, FP64.  A "step"
+is one pass of the hot path (boysfn_eval_device) over that batch; x is the
+splitmix64 stream of boysfn_generate_uniform (seed 2), rank r taking global
+indices [r*N, (r+1)*N) -- weak scaling, no collective on the data path (the
+only NCCL calls are the timing barrier and the max-over-ranks reduction).
+
+Reported beside `value` (device-resident, CUDA events on the launching stream):
+  e2e          same metric through the reference-facing host API
+               (boysfn_eval_host, pinned host buffers, H2D of x and D2H of all
+               F values inside the timed region)
+  roofline     algorithmic bytes per launch (8 B read + 8(k+1) B written per x)
+               / mean launch time, against MEASURED_PEAKS.json hbm_gbs; traffic
+               from the committed ncu capture (profiles/ncu_summary.json)
+  cpu_baseline the unmodified reference (oracle/_ref) on all host cores over a
+               bounded sample of the same stream (rank 0, N=1 only)
+  accuracy     max |F - oracle| on a sample (binary128 oracle, oracle/boys_hp.c)
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Boys values/sec (F_k·x) at kmax=8/32, 1/2/4/8 B200; %FP64/HBM roofline; max abs err"
+UNIT = "values/s"
+WORKLOAD = "configs[1]: F_0..F_32 for 1e8 uniform x in [0,100] per B200, SoA output, FP64"
+SEED = 2
+LO, HI = 0.0, 100.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=float, default=1e8, help="x values per GPU")
+    ap.add_argument("--k", type=int, default=32)
+    ap.add_argument("--layout", default="soa", choices=["soa", "aos"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
+    a = ap.parse_args()
+    a.warmup = max(a.warmup, 3)
+    a.n = int(a.n)
+    return a
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(k, layout):
+    """dram bytes per launch from the committed ncu --set full capture, if it
+    was taken on this workload (profiles/ncu_summary.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        e = s["launches"].get("%s_k%d" % (layout, k))
+        return e["dram_bytes_per_launch"] if e else None
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [v.strip() for v in line.split(",")]
+            if len(f) == 7:
+                self.rows.append(f)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4) if r[3 + j] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def init_dist(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference(n_sample, k, threads, min_seconds=2.0):
+    """The unmodified reference (oracle/_ref, else the C restatement) on
+    `threads` host threads over the first n_sample x of the workload stream,
+    repeated until min_seconds elapsed.  Returns (values/s, kind, sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import pyoracle
+    port = pyoracle.Port()
+    xs = port.gen_uniform(n_sample, SEED, LO, HI)  # bit-identical to the device stream
+    if pyoracle.Ref.available():
+        ref, kind = pyoracle.Ref(), "reference"
+        run = lambda out: ref.boys_batch_many_mt(xs, k, threads, out=out)  # noqa: E731
+    else:
+        kind = "port"
+        run = lambda out: port.boys_batch_many(xs, k, threads=threads)  # noqa: E731
+    out = np.empty(n_sample * (k + 1))
+    run(out)  # warm (page faults)
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        run(out)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds:
+            break
+    value = passes * n_sample * (k + 1) / el
+    sample = ("%d pass(es) over the first %d x of the workload stream (U[0,100], seed %d), k=%d, AoS, "
+              "%d thread(s), %.2f s" % (passes, n_sample, SEED, k, threads, el))
+    return value, kind, sample
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_sample = min(args.n, 4_000_000)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, kind, sample = cpu_reference(n_sample, args.k, threads, min_seconds=0.5)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * n_sample * (args.k + 1) / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "kmax": args.k, "layout": "aos (reference API)",
+                   "n_per_step": n_sample, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def accuracy_sample(x_dev, k, layout, n):
+    """max |gpu - oracle| and |gpu - reference| on a strided sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import torch
+    import pyoracle
+    import paper_2512_10059_b200 as pkg
+    m = 20000
+    m = min(m, n)
+    idx = torch.arange(m, device=x_dev.device, dtype=torch.int64) * (n // m)
+    xs = x_dev[idx].contiguous()
+    out = torch.empty(m * (k + 1), dtype=torch.float64, device=x_dev.device)
+    pkg.eval_device(xs, k, out, layout=layout)
+    g = out.view(k + 1, m).T.cpu().numpy() if layout == "soa" else out.view(m, k + 1).cpu().numpy()
+    port = pyoracle.Port()
+    xh = xs.cpu().numpy()
+    hp = port.hp(xh, k)
+    ref = port.boys_batch_many(xh, k)
+    return {"max_abs_err_vs_oracle": float(np.abs(g - hp).max()),
+            "max_abs_dev_vs_reference": float(np.abs(g - ref).max()),
+            "eps_tol": 5e-14, "sample": "%d x strided over the timed batch, all orders 0..%d" % (m, k)}
+
+
+def run_b200(args, world, rank, local):
+    import numpy as np
+    import torch
+    import paper_2512_10059_b200 as pkg
+
+    dev = torch.device("cuda", local if world > 1 else 0)
+    n, k = args.n, args.k
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    pkg.generate_uniform(x, SEED, LO, HI, offset=rank * n)
+    out = torch.empty(n * (k + 1), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        pkg.eval_device(x, k, out, layout=args.layout)
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(dev.index if world == 1 else local)
+    sampler.start()
+    time.sleep(0.1)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    launches0 = pkg.kernel_launch_count()
+    ev[0].record(stream)
+    for s in range(args.steps):
+        pkg.eval_device(x, k, out, layout=args.layout)
+        ev[s + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    launches = pkg.kernel_launch_count() - launches0
+    clocks = sampler.stop()
+    total_ms = ev[0].elapsed_time(ev[-1])
+    per_launch = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
+    total_ms = max_over_ranks(total_ms, world)
+    ms_step = total_ms / args.steps
+    value = world * n * (k + 1) / (ms_step * 1e-3)
+
+    hbm, peak_kind = peaks()
+    alg_bytes = n * (8 + 8 * (k + 1))
+    mean_launch_s = statistics.mean(per_launch) * 1e-3
+    achieved = alg_bytes / mean_launch_s / 1e9
+    traffic = ncu_traffic(k, args.layout)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "note": "per x: 8 B read + 8*(k+1) B written; one launch per step"}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, x, rank, world)
+
+    acc = None
+    if rank == 0 and not args.no_accuracy:
+        acc = accuracy_sample(x, k, args.layout, n)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, kind, sample = cpu_reference(min(n, 4_000_000), k, threads, min_seconds=2.0)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_per_gpu": n, "kmax": k, "layout": args.layout,
+                       "x": "U[%g,%g] splitmix64 seed %d, global index offset rank*N" % (LO, HI, SEED),
+                       "l2": "inputs+outputs %.1f GB per step >> 126 MB L2 (no flush needed)"
+                             % (alg_bytes / 1e9),
+                       "parallelism": "dp%d (independent shards, no collective)" % world},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "accuracy": acc,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, x_dev, rank, world):
+    """Same metric through the host API: pinned host x -> device -> pinned host F."""
+    import numpy as np
+    import torch
+    import paper_2512_10059_b200 as pkg
+    n, k = args.n, args.k
+    hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    hx.copy_(x_dev.cpu() if n <= 10_000_000 else x_dev.to("cpu"))
+    hout = torch.empty(n * (k + 1), dtype=torch.float64, pin_memory=True)
+    xs, out = hx.numpy(), hout.numpy()
+    tables = pkg.embedded_default()
+    lay = args.layout
+    pkg.boys_batch_many(xs, k, tables, out, layout=lay)  # warm (pipeline buffers)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        pkg.boys_batch_many(xs, k, tables, out, layout=lay)
+    el = time.perf_counter() - t0
+    barrier(world)
+    el = max_over_ranks(el, world)
+    v = world * n * (k + 1) * args.e2e_steps / el
+    return {"value": v, "unit": UNIT, "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * (k + 1) * 8,
+            "steps": args.e2e_steps, "api": "boys_batch_many -> boysfn_eval_host (pinned host buffers)",
+            "layout": lay}
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference_arm(args, world, rank)
+        return
+    world, rank, local = init_dist(args)
+    try:
+        run_b200(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -202,8 +202,16 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
   EvalParams p = t->params[k];
   p.force_region = force_region;
-  void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad};
-  CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, smem, stream));
+  // Per-launch tile counter from the stream-ordered pool: zeroed, used and
+  // released in stream order, so concurrent launches on other streams never
+  // share it.
+  unsigned long long* counter = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), stream));
+  CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
+  void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad, &counter};
+  const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, smem, stream);
+  CUDA_TRY(cudaFreeAsync(counter, stream));
+  if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return BOYSFN_OK;
 }

@@ -16,7 +16,7 @@
  *  - series length (reference.cpp:46-54, reference_terms_for): smallest
  *    multiple-of-25 L >= 150 whose bound x^{k+L+3/2}/Gamma(k+L+3/2) <= rel.
  *    The reference throws above x ~ 7331 (cap L <= 20000); there, and for any
- *    x >= kClosedFormX, F_kmax comes from the closed form
+ *    x >= max(kClosedFormX, kmax + 12), F_kmax comes from the closed form
  *    F_k(x) = [Gamma(k+1/2) - Gamma(k+1/2, x)] / (2 x^{k+1/2}),
  *    with Gamma(a, x) by the modified-Lentz continued fraction the reference
  *    uses for erfc (highprec.cpp:95-117).  tests/test_oracle.py checks that the
@@ -116,9 +116,11 @@ int oracle_hp_boys_batch(int kmax, double xd, double* out) {
   }
   const q_t x = (q_t)xd;
   q_t fk;
-  if (xd < kClosedFormX) {
+  /* The continued fraction for Gamma(a, x) needs x comfortably above a + 1. */
+  if (xd < kClosedFormX || xd < kmax + 12.0) {
     /* verify.cpp:35 sizes L at k = 0 (conservative); 1e-30 target as there. */
     const int L = oracle_hp_terms_for(0, xd, 1e-30);
+    if (L < 0) return ORACLE_ERR_RANGE;
     fk = hp_series_q(kmax, x, L);
   } else {
     fk = hp_closed_form_q(kmax, x);

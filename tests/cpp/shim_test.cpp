@@ -152,7 +152,8 @@ int cmd_gpu() {
     CHECK(boysfn::classify_region(std::nextafter(T.x0, 0.0), T) == boysfn::Region::A, "x0- -> A");
     CHECK(boysfn::classify_region(T.x1, T) == boysfn::Region::C, "x1 -> C");
     for (int r = 0; r < 3; ++r) {
-      const double x = T.x1 + 1e-9;
+      // each forced region at a point of its own interval's closure
+      const double x = r == 0 ? T.x0 - 1e-9 : r == 1 ? T.x0 + 1e-9 : T.x1 + 1e-9;
       const auto g = boysfn::boys_batch_region(x, 20, T, static_cast<boysfn::Region>(r));
       std::vector<double> w(21);
       oracle_boys_batch_region(x, 20, &O.t, r, w.data());

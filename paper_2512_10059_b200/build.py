@@ -29,7 +29,8 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra"]
 
-CU_SOURCES = ["kernels_soa.cu", "kernels_aos_tma.cu", "kernels_aos_xpose.cu", "capi.cu"]
+CU_SOURCES = ["kernels_soa.cu", "kernels_aos_tma.cu", "kernels_aos_xpose.cu", "kernels_soa_block.cu",
+              "kernels_aos_block.cu", "kernels_soa_binned.cu", "kernels_aos_binned.cu", "capi.cu"]
 CPP_SOURCES = ["shim_tables.cpp", "shim_eval.cpp"]
 
 
@@ -57,7 +58,15 @@ def _headers():
     return hs
 
 
-def build_library(force=False, verbose=True):
+def build_library(force=False, verbose=True, variant=None, defines=()):
+    """variant/defines: an experimental build into _lib/variants/<variant>/
+    (selected at run time with BOYSFN_LIB); the product build has neither."""
+    global OBJ, LIB
+    if variant:
+        OBJ = os.path.join(ROOT, "build", "obj_" + variant)
+        LIB = os.path.join(LIBDIR, "variants", variant, "libboysfn_b200.so")
+        os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    extra = ["-D" + d for d in defines]
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
     hdrs = _headers()
@@ -66,7 +75,7 @@ def build_library(force=False, verbose=True):
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         if force or _stale(o, [s] + hdrs):
-            jobs.append(([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], os.path.join(OBJ, src + ".ptxas.log")))
+            jobs.append(([NVCC] + NVCC_FLAGS + extra + ["-c", s, "-o", o], os.path.join(OBJ, src + ".ptxas.log")))
     for src in CPP_SOURCES:
         s = os.path.join(CPP, "src", src)
         o = os.path.join(OBJ, src + ".o")
@@ -109,4 +118,8 @@ def build_all(force=False):
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        build_library(force=True, variant=sys.argv[i + 1], defines=sys.argv[i + 2:])
+    else:
+        build_all(force="--force" in sys.argv)

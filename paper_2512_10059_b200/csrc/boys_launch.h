@@ -20,6 +20,10 @@ constexpr int kKernelKmax = 32;
 const void* kernel_soa(int k, int variant);
 const void* kernel_aos_tma(int k, int variant);
 const void* kernel_aos_xpose(int k, int variant);
+const void* kernel_soa_block(int k, int variant);
+const void* kernel_aos_block(int k, int variant);
+const void* kernel_soa_binned(int k, int variant);
+const void* kernel_aos_binned(int k, int variant);
 
 // Exact degrees of the embedded kernels (from embedded_tables.inc).
 void embedded_degrees(int k, int* na, int* ma, int* nb, int* mb);

@@ -157,6 +157,8 @@ int occupancy(const void* fn, size_t smem, int* sms, int* bps) {
   if (di.sms == 0) CUDA_TRY(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
   auto it = di.blocks_per_sm.find(fn);
   if (it == di.blocks_per_sm.end()) {
+    if (smem > 48 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int b = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, boysfn_dev::kThreadsPerBlock, smem));
     it = di.blocks_per_sm.emplace(fn, std::max(b, 1)).first;
@@ -166,12 +168,32 @@ int occupancy(const void* fn, size_t smem, int* sms, int* bps) {
   return BOYSFN_OK;
 }
 
-bool force_xpose() {
-  static const bool v = [] {
-    const char* e = std::getenv("BOYSFN_AOS_PATH");
-    return e != nullptr && std::strcmp(e, "xpose") == 0;
-  }();
-  return v;
+// Output-path selection (medians of interleaved
+// B200 runs in profiles/r01_paths.txt):
+//   k <= 8   region-binned kernels: the per-x work is short, so divergence
+//            between the A/B/C paths made the per-warp kernels issue-bound;
+//   k >= 9   per-warp kernels: SoA lane-contiguous rows; AoS through the TMA
+//            bulk store when k+1 is odd and the output 16-B aligned, else the
+//            shared-memory transpose.
+// BOYSFN_SOA_PATH = warp|block|binned and BOYSFN_AOS_PATH = tma|xpose|block|binned
+// override the choice (experiments, and the path-equivalence tests).
+int choose_store(int layout, int k, const double* d_out) {
+  const int R = k + 1;
+  const char* e = std::getenv(layout == BOYSFN_LAYOUT_SOA ? "BOYSFN_SOA_PATH" : "BOYSFN_AOS_PATH");
+  const std::string want = e ? e : "";
+  const bool tma_ok = (R & 1) && (reinterpret_cast<uintptr_t>(d_out) & 15) == 0;
+  if (layout == BOYSFN_LAYOUT_SOA) {
+    if (want == "warp") return boysfn_dev::kStoreSoA;
+    if (want == "block") return boysfn_dev::kStoreSoABlock;
+    if (want == "binned") return boysfn_dev::kStoreSoABinned;
+    return k <= 8 ? boysfn_dev::kStoreSoABinned : boysfn_dev::kStoreSoA;
+  }
+  if (want == "tma" && tma_ok) return boysfn_dev::kStoreAoSTma;
+  if (want == "xpose") return boysfn_dev::kStoreAoSXpose;
+  if (want == "block") return (R & 1) ? boysfn_dev::kStoreAoSBlock : boysfn_dev::kStoreAoSXpose;
+  if (want == "binned") return boysfn_dev::kStoreAoSBinned;
+  if (k <= 8) return boysfn_dev::kStoreAoSBinned;
+  return tma_ok ? boysfn_dev::kStoreAoSTma : boysfn_dev::kStoreAoSXpose;
 }
 
 // Launches the evaluation kernel; k already validated against the handle.
@@ -184,16 +206,37 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   if (!t->degree_ok[k])
     return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
   const int R = k + 1;
+  const int v = t->variant[k];
   const void* fn = nullptr;
   size_t smem = 0;
-  if (layout == BOYSFN_LAYOUT_SOA) {
-    fn = boysfn_dev::kernel_soa(k, t->variant[k]);
-  } else if ((R & 1) && (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && !force_xpose()) {
-    fn = boysfn_dev::kernel_aos_tma(k, t->variant[k]);
-    smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * 32 * R;
-  } else {
-    fn = boysfn_dev::kernel_aos_xpose(k, t->variant[k]);
-    smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::kXposePitch * R;
+  switch (choose_store(layout, k, d_out)) {
+    case boysfn_dev::kStoreSoA:
+      fn = boysfn_dev::kernel_soa(k, v);
+      break;
+    case boysfn_dev::kStoreAoSTma:
+      fn = boysfn_dev::kernel_aos_tma(k, v);
+      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * 32 * R;
+      break;
+    case boysfn_dev::kStoreAoSXpose:
+      fn = boysfn_dev::kernel_aos_xpose(k, v);
+      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::kXposePitch * R;
+      break;
+    case boysfn_dev::kStoreSoABlock:
+      fn = boysfn_dev::kernel_soa_block(k, v);
+      smem = sizeof(double) * boysfn_dev::kBlockX * R;
+      break;
+    case boysfn_dev::kStoreAoSBlock:
+      fn = boysfn_dev::kernel_aos_block(k, v);
+      smem = sizeof(double) * boysfn_dev::kBlockX * R;
+      break;
+    case boysfn_dev::kStoreSoABinned:
+      fn = boysfn_dev::kernel_soa_binned(k, v);
+      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * (R * boysfn_dev::kBinX + boysfn_dev::kBinX * 3 / 2);
+      break;
+    default:
+      fn = boysfn_dev::kernel_aos_binned(k, v);
+      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * (R * boysfn_dev::kBinX + boysfn_dev::kBinX * 3 / 2);
+      break;
   }
   int sms = 0, bps = 0;
   if (int st = occupancy(fn, smem, &sms, &bps)) return st;

@@ -1,0 +1,54 @@
+"""Every output path (per-warp SoA/AoS-TMA/AoS-transpose, block-tile, and
+region-binned kernels) computes each value with the same arithmetic routine, so
+all must agree BIT FOR BIT with one another -- on ragged sizes around the 32-x
+tile, 128-x block and 512-x chunk edges and for every order 0..32.  The default
+selection is covered by test_gpu_parity.py against the oracle."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2512_10059_b200 as pkg
+
+pytestmark = pytest.mark.gpu
+
+PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("aos", "tma"), ("aos", "xpose"),
+         ("aos", "block"), ("aos", "binned")]
+
+
+def run(torch, x, k, lay, path, monkeypatch):
+    monkeypatch.setenv("BOYSFN_SOA_PATH" if lay == "soa" else "BOYSFN_AOS_PATH", path)
+    n = x.numel()
+    out = torch.full((n * (k + 1),), float("nan"), dtype=torch.float64, device="cuda")
+    pkg.eval_device(x, k, out, layout=lay)
+    torch.cuda.synchronize()
+    monkeypatch.delenv("BOYSFN_SOA_PATH", raising=False)
+    monkeypatch.delenv("BOYSFN_AOS_PATH", raising=False)
+    return out.view(k + 1, n).T.contiguous() if lay == "soa" else out.view(n, k + 1)
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 127, 128, 129, 511, 513, 4099, 200_003])
+def test_all_paths_bit_identical(cuda, monkeypatch, n):
+    torch = cuda
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    pkg.generate_uniform(x, 100 + n, 0.0, 45.0)
+    ks = range(33) if n in (129, 4099) else (0, 1, 4, 8, 9, 16, 31, 32)
+    for k in ks:
+        ref = run(torch, x, k, "soa", "warp", monkeypatch).view(torch.int64)
+        for lay, path in PATHS[1:]:
+            got = run(torch, x, k, lay, path, monkeypatch).view(torch.int64)
+            assert torch.equal(got, ref), (n, k, lay, path)
+
+
+def test_binned_paths_report_first_bad(cuda, port):
+    torch = cuda
+    xs = port.gen_uniform(5000, 3, 0.0, 30.0)
+    xs[4321] = np.inf
+    xs[777] = -3.0
+    x = torch.from_numpy(xs).cuda()
+    for k in (0, 4, 8):  # the binned kernels are the default for k <= 8
+        for lay in ("soa", "aos"):
+            fb = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+            out = torch.empty(xs.size * (k + 1), dtype=torch.float64, device="cuda")
+            pkg.eval_device(x, k, out, layout=lay, first_bad=fb)
+            assert int(fb.item()) == 777

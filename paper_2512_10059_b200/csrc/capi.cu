@@ -2,6 +2,7 @@
 // dispatch, the chunked host<->device pipeline behind boys_batch_many, and the
 // synthetic-workload generators.  Every evaluation runs on the GPU; there is no
 // CPU fallback: without a device the calls return BOYSFN_ERR_CUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -168,32 +169,72 @@ int occupancy(const void* fn, size_t smem, int* sms, int* bps) {
   return BOYSFN_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2D map over the SoA output: dim0 = x index (n, contiguous), dim1 = order
+// (k+1 rows, stride ld); box = one block tile, 128 x by k+1 rows.
+bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R) {
+  EncodeTiledFn enc = encode_tiled();
+  if (enc == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) || (ld * sizeof(double)) % 16 ||
+      n > (size_t(1) << 31) - 256)
+    return false;
+  const cuuint64_t dims[2] = {n, static_cast<cuuint64_t>(R)};
+  const cuuint64_t strides[1] = {ld * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(boysfn_dev::kBlockX), static_cast<cuuint32_t>(R)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Output-path selection (medians of interleaved
-// B200 runs in profiles/r01_paths.txt):
-//   k <= 8   region-binned kernels: the per-x work is short, so divergence
-//            between the A/B/C paths made the per-warp kernels issue-bound;
-//   k >= 9   per-warp kernels: SoA lane-contiguous rows; AoS through the TMA
-//            bulk store when k+1 is odd and the output 16-B aligned, else the
-//            shared-memory transpose.
-// BOYSFN_SOA_PATH = warp|block|binned and BOYSFN_AOS_PATH = tma|xpose|block|binned
-// override the choice (experiments, and the path-equivalence tests).
+// B200 runs, profiles/r01_paths*.txt).  Large k is HBM-write-bound and wants
+// long contiguous write bursts: block tiles of 128 x stored by the TMA engine
+// (1 KB SoA row segments / 1 KB*(k+1) AoS spans).  Small k is issue-bound
+// and wants no A/B/C divergence: the region-binned kernels.  AoS with k+1
+// even avoids the block stage (bank conflicts on the row-major stage) and uses
+// the per-warp transpose path.
+//   SoA: k <= 6 binned, else block-TMA (block/LSU if no tensor map applies)
+//   AoS: k <= 6 or k == 8 binned; k+1 odd block-TMA; k+1 even transpose
+// BOYSFN_SOA_PATH = warp|block|binned|blocktma and
+// BOYSFN_AOS_PATH = tma|xpose|block|binned|blocktma override the choice
+// (experiments and the path-equivalence tests).
 int choose_store(int layout, int k, const double* d_out) {
   const int R = k + 1;
   const char* e = std::getenv(layout == BOYSFN_LAYOUT_SOA ? "BOYSFN_SOA_PATH" : "BOYSFN_AOS_PATH");
   const std::string want = e ? e : "";
-  const bool tma_ok = (R & 1) && (reinterpret_cast<uintptr_t>(d_out) & 15) == 0;
+  const bool a16 = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0;
   if (layout == BOYSFN_LAYOUT_SOA) {
     if (want == "warp") return boysfn_dev::kStoreSoA;
     if (want == "block") return boysfn_dev::kStoreSoABlock;
     if (want == "binned") return boysfn_dev::kStoreSoABinned;
-    return k <= 8 ? boysfn_dev::kStoreSoABinned : boysfn_dev::kStoreSoA;
+    if (want == "blocktma") return boysfn_dev::kStoreSoABlockTma;
+    return k <= 6 ? boysfn_dev::kStoreSoABinned : boysfn_dev::kStoreSoABlockTma;
   }
-  if (want == "tma" && tma_ok) return boysfn_dev::kStoreAoSTma;
+  if (want == "tma" && (R & 1) && a16) return boysfn_dev::kStoreAoSTma;
   if (want == "xpose") return boysfn_dev::kStoreAoSXpose;
-  if (want == "block") return (R & 1) ? boysfn_dev::kStoreAoSBlock : boysfn_dev::kStoreAoSXpose;
+  if (want == "block") return boysfn_dev::kStoreAoSBlock;
   if (want == "binned") return boysfn_dev::kStoreAoSBinned;
-  if (k <= 8) return boysfn_dev::kStoreAoSBinned;
-  return tma_ok ? boysfn_dev::kStoreAoSTma : boysfn_dev::kStoreAoSXpose;
+  if (want == "blocktma" && a16) return boysfn_dev::kStoreAoSBlockTma;
+  if (!want.empty()) return boysfn_dev::kStoreAoSXpose;
+  if (k <= 6 || k == 8) return boysfn_dev::kStoreAoSBinned;
+  if ((R & 1) && a16) return boysfn_dev::kStoreAoSBlockTma;
+  return boysfn_dev::kStoreAoSXpose;
 }
 
 // Launches the evaluation kernel; k already validated against the handle.
@@ -209,7 +250,20 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   const int v = t->variant[k];
   const void* fn = nullptr;
   size_t smem = 0;
-  switch (choose_store(layout, k, d_out)) {
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof tmap);
+  int store = choose_store(layout, k, d_out);
+  if (store == boysfn_dev::kStoreSoABlockTma && !make_soa_tmap(&tmap, d_out, n, ld, R))
+    store = boysfn_dev::kStoreSoABlock;
+  switch (store) {
+    case boysfn_dev::kStoreSoABlockTma:
+      fn = boysfn_dev::kernel_soa_block_tma(k, v);
+      smem = sizeof(double) * boysfn_dev::kBlockX * R + 16;
+      break;
+    case boysfn_dev::kStoreAoSBlockTma:
+      fn = boysfn_dev::kernel_aos_block_tma(k, v);
+      smem = sizeof(double) * boysfn_dev::kBlockX * R + 16;
+      break;
     case boysfn_dev::kStoreSoA:
       fn = boysfn_dev::kernel_soa(k, v);
       break;
@@ -251,7 +305,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   unsigned long long* counter = nullptr;
   CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), stream));
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
-  void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad, &counter};
+  void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad, &counter, &tmap};  // tmap: block-TMA kernels only
   const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, smem, stream);
   CUDA_TRY(cudaFreeAsync(counter, stream));
   if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");

@@ -12,8 +12,8 @@ import paper_2512_10059_b200 as pkg
 
 pytestmark = pytest.mark.gpu
 
-PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("aos", "tma"), ("aos", "xpose"),
-         ("aos", "block"), ("aos", "binned")]
+PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("aos", "tma"),
+         ("aos", "xpose"), ("aos", "block"), ("aos", "binned"), ("aos", "blocktma")]
 
 
 def run(torch, x, k, lay, path, monkeypatch):

@@ -150,7 +150,7 @@ struct DeviceInfo {
 std::mutex g_dev_mu;
 std::map<int, DeviceInfo> g_devices;
 
-int occupancy(const void* fn, size_t smem, int* sms, int* bps) {
+int occupancy(const void* fn, int threads, size_t smem, int* sms, int* bps) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_dev_mu);
@@ -161,7 +161,7 @@ int occupancy(const void* fn, size_t smem, int* sms, int* bps) {
     if (smem > 48 * 1024)
       CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int b = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, boysfn_dev::kThreadsPerBlock, smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem));
     it = di.blocks_per_sm.emplace(fn, std::max(b, 1)).first;
   }
   *sms = di.sms;
@@ -188,14 +188,14 @@ EncodeTiledFn encode_tiled() {
 
 // 2D map over the SoA output: dim0 = x index (n, contiguous), dim1 = order
 // (k+1 rows, stride ld); box = one block tile, 128 x by k+1 rows.
-bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R) {
+bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R, int box_x) {
   EncodeTiledFn enc = encode_tiled();
   if (enc == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) || (ld * sizeof(double)) % 16 ||
       n > (size_t(1) << 31) - 256)
     return false;
   const cuuint64_t dims[2] = {n, static_cast<cuuint64_t>(R)};
   const cuuint64_t strides[1] = {ld * sizeof(double)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(boysfn_dev::kBlockX), static_cast<cuuint32_t>(R)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_x), static_cast<cuuint32_t>(R)};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -253,7 +253,8 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
   int store = choose_store(layout, k, d_out);
-  if (store == boysfn_dev::kStoreSoABlockTma && !make_soa_tmap(&tmap, d_out, n, ld, R))
+  const int threads = boysfn_dev::kThreadsPerBlock;
+  if (store == boysfn_dev::kStoreSoABlockTma && !make_soa_tmap(&tmap, d_out, n, ld, R, threads))
     store = boysfn_dev::kStoreSoABlock;
   switch (store) {
     case boysfn_dev::kStoreSoABlockTma:
@@ -293,9 +294,10 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
       break;
   }
   int sms = 0, bps = 0;
-  if (int st = occupancy(fn, smem, &sms, &bps)) return st;
+  if (int st = occupancy(fn, threads, smem, &sms, &bps)) return st;
   const size_t ntiles = (n + 31) / 32;
-  const size_t want = (ntiles + boysfn_dev::kWarpsPerBlock - 1) / boysfn_dev::kWarpsPerBlock;
+  const size_t wpb = static_cast<size_t>(threads / 32);
+  const size_t want = (ntiles + wpb - 1) / wpb;
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
   EvalParams p = t->params[k];
   p.force_region = force_region;
@@ -306,7 +308,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), stream));
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
   void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad, &counter, &tmap};  // tmap: block-TMA kernels only
-  const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, smem, stream);
+  const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
   CUDA_TRY(cudaFreeAsync(counter, stream));
   if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise an `ncu --set full` report into profiles/ (text + ncu_summary.json).
 
-    python tools/ncu_summarize.py gpurun_out/prof.ncu-rep <key> <out.txt>
+    python tools/ncu_summarize.py gpurun_out/prof.ncu-rep <key> <out.txt> [n]
 
 <key> names the workload (e.g. soa_k32); ncu_summary.json[launches][key] gets
 the per-launch DRAM traffic that bench.py reports as roofline.traffic.
@@ -35,6 +35,7 @@ def raw(rep):
 
 def main():
     rep, key, txt = sys.argv[1], sys.argv[2], sys.argv[3]
+    n_x = int(float(sys.argv[4])) if len(sys.argv) > 4 else None
     h, u, data = raw(rep)
     lines = []
     summary = None
@@ -66,6 +67,8 @@ def main():
                    "dram_bytes_read": num("dram__bytes_read.sum"), "dram_bytes_write": num("dram__bytes_write.sum"),
                    "report": os.path.basename(rep)}
         summary["dram_bytes_per_launch"] = summary["dram_bytes_read"] + summary["dram_bytes_write"]
+        if n_x:
+            summary["n"] = n_x
     with open(txt, "w") as f:
         f.write("# ncu --set full --clock-control none (%s); per-launch values, cold cache, serialised\n" % rep)
         f.write("\n".join(lines) + "\n")

@@ -8,6 +8,7 @@ that batch; x is the splitmix64 stream of boysfn_generate_uniform (seed 2), rank
 r taking global indices [r*N, (r+1)*N) -- weak scaling, no collective on the
 data path (the only NCCL calls are the timing barrier and the max-over-ranks
 reduction).  Other named configs (reported in DESIGN.md, not the driver's line):
+  cfg2       configs[2]: 1e8 x clustered at the region boundaries, k = 0..32 sweep
   cfg3       configs[3]: 1e9 log-uniform x in [1e-12, 1e4], k = 16, AoS (fits HBM)
   northstar  1e9 uniform x in [0,100], k = 32, SoA, streamed through a reused
              1e8-x output buffer (264 GB of F per step > HBM)
@@ -45,6 +46,10 @@ CONFIGS = {
                  n=100_000_000, k=32, layout="soa", dist="uniform", lo=0.0, hi=100.0, seed=2, chunk=None),
     "cfg3": dict(workload="configs[3]: ERI-like F_0..F_16 for 1e9 log-uniform x in [1e-12,1e4] per B200, AoS",
                  n=1_000_000_000, k=16, layout="aos", dist="loguniform", lo=-12.0, hi=4.0, seed=4, chunk=None),
+    "cfg2": dict(workload="configs[2]: region-boundary stress, 1e8 x clustered at 0+/x0/x1 and mixed per warp, "
+                          "kmax 0..32 sweep (one launch per k per step), SoA",
+                 n=100_000_000, k=32, ks=list(range(33)), layout="soa", dist="boundary", lo=0.0, hi=0.0, seed=3,
+                 chunk=None),
     "northstar": dict(workload="north star: F_0..F_32 for 1e9 uniform x in [0,100] per B200, SoA, streamed "
                                "through a reused 1e8-x output buffer (264 GB of F per step > HBM)",
                       n=1_000_000_000, k=32, layout="soa", dist="uniform", lo=0.0, hi=100.0, seed=2,
@@ -150,6 +155,8 @@ class ClockSampler:
 def generate(pkg, x, cfg, offset):
     if cfg["dist"] == "uniform":
         pkg.generate_uniform(x, cfg["seed"], cfg["lo"], cfg["hi"], offset=offset)
+    elif cfg["dist"] == "boundary":
+        pkg.generate_boundary(x, cfg["seed"], offset=offset)
     else:
         pkg.generate_loguniform(x, cfg["seed"], cfg["lo"], cfg["hi"], offset=offset)
 
@@ -188,6 +195,17 @@ def reference_sample(cfg, m):
     port = pyoracle.Port()
     if cfg["dist"] == "uniform":
         return port.gen_uniform(m, cfg["seed"], cfg["lo"], cfg["hi"])
+    if cfg["dist"] == "boundary":  # same clustering law on the host
+        import numpy as np
+        rng = np.random.default_rng(cfg["seed"])
+        b = np.array([0.0, port.x0, port.x1])[rng.integers(0, 3, m)]
+        mode = rng.integers(0, 3, m)
+        j = rng.integers(-64, 65, m).astype(np.float64)
+        ulp = np.where(b == 0.0, 5e-324, np.spacing(np.maximum(b, 1e-300)))
+        v = np.where(mode == 0, b + j * ulp,
+                     np.where(mode == 1, b + rng.choice([-1.0, 1.0], m) * 10.0 ** -rng.uniform(1, 15, m),
+                              b + rng.uniform(-1, 1, m)))
+        return np.abs(v)
     u = port.gen_uniform(m, cfg["seed"], 0.0, 1.0)
     return 10.0 ** (cfg["lo"] + (cfg["hi"] - cfg["lo"]) * u)
 
@@ -197,12 +215,17 @@ def run_reference_arm(args):
     threads = os.cpu_count() or 1
     n_sample = min(cfg["n"], 4_000_000)
     xs = reference_sample(cfg, n_sample)
+    ks = cfg.get("ks") or [k]
     vals = []
     kind = "reference"
     for i in range(args.warmup + args.steps):
-        v, kind, passes, el = cpu_reference(xs, k, threads, min_seconds=0.5)
+        t_all, v_all = 0.0, 0.0
+        for kk in ks:
+            v, kind, passes, el = cpu_reference(xs, kk, threads, min_seconds=0.5 / len(ks))
+            t_all += el
+            v_all += v * el
         if i >= args.warmup:
-            vals.append(v)
+            vals.append(v_all / t_all)
     value = statistics.mean(vals)
     sample = ("each step: passes over the first %d x of the workload stream until >= 0.5 s, k=%d, AoS, "
               "%d threads" % (n_sample, k, threads))
@@ -256,10 +279,20 @@ def run_b200(args, world, rank, local):
     out = torch.empty(chunk * (k + 1), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     pieces = [(c, min(n, c + chunk)) for c in range(0, n, chunk)]
+    ks = cfg.get("ks") or [k]
+    launch_ev = {}
 
-    def step():
-        for c0, c1 in pieces:
-            pkg.eval_device(x[c0:c1], k, out[: (c1 - c0) * (k + 1)], layout=layout)
+    def step(record=False):
+        for kk in ks:
+            for c0, c1 in pieces:
+                if record:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                pkg.eval_device(x[c0:c1], kk, out[: (c1 - c0) * (kk + 1)], layout=layout)
+                if record:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(stream)
+                    launch_ev.setdefault(kk, []).append((e0, e1))
 
     for _ in range(args.warmup):
         step()
@@ -274,7 +307,7 @@ def run_b200(args, world, rank, local):
     launches0 = pkg.kernel_launch_count()
     ev[0].record(stream)
     for s in range(args.steps):
-        step()
+        step(record=len(ks) > 1)
         ev[s + 1].record(stream)
     torch.cuda.synchronize(dev)
     D.barrier()
@@ -283,19 +316,32 @@ def run_b200(args, world, rank, local):
     total_ms = D.max_over_ranks(ev[0].elapsed_time(ev[-1]))
     per_step = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
     ms_step = total_ms / args.steps
-    value = world * n * (k + 1) / (ms_step * 1e-3)
+    values_per_step = n * sum(kk + 1 for kk in ks)
+    value = world * values_per_step / (ms_step * 1e-3)
 
     hbm, peak_kind = peaks()
     alg_bytes = chunk * (8 + 8 * (k + 1))
-    mean_launch_s = statistics.mean(per_step) * 1e-3 / len(pieces)
+    if len(ks) > 1:  # sweep: algorithmic bytes of the whole step over its time
+        alg_bytes = sum(n * (8 + 8 * (kk + 1)) for kk in ks)
+        mean_launch_s = statistics.mean(per_step) * 1e-3
+    else:
+        mean_launch_s = statistics.mean(per_step) * 1e-3 / len(pieces)
     achieved = alg_bytes / mean_launch_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": ncu_traffic(cfg), "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "note": "per x: 8 B read + 8*(k+1) B written; %d launch(es) per step" % len(pieces)}
 
+    per_k = None
+    if len(ks) > 1:
+        per_k = {}
+        for kk, evs in launch_ev.items():
+            ms = statistics.median(a.elapsed_time(b) for a, b in evs)
+            gbs = n * (8 + 8 * (kk + 1)) / (ms * 1e-3) / 1e9
+            per_k[kk] = {"values_per_s": n * (kk + 1) / (ms * 1e-3), "ms": ms, "hbm_frac": gbs / hbm}
+
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and len(ks) == 1:
         e2e = run_e2e(args, x, world)
 
     acc = None
@@ -307,10 +353,14 @@ def run_b200(args, world, rank, local):
         threads = os.cpu_count() or 1
         m = min(n, 4_000_000)
         xs = x[:m].cpu().numpy()  # the exact doubles the GPU evaluated
-        v, kind, passes, el = cpu_reference(xs, k, threads, min_seconds=2.0)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": "%d pass(es) over the first %d x of the timed batch, k=%d, AoS, %d threads, %.2f s"
-                         % (passes, m, k, threads, el)}
+        t_all = v_all = 0.0
+        for kk in ks:  # time-weighted over the sweep (one k unless cfg2)
+            v, kind, passes, el = cpu_reference(xs, kk, threads, min_seconds=2.0 / len(ks))
+            t_all += el
+            v_all += v * el
+        cpu = {"value": v_all / t_all, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": "first %d x of the timed batch, k in %s, AoS, %d threads, %.2f s"
+                         % (m, "0..%d" % max(ks) if len(ks) > 1 else str(k), threads, t_all)}
 
     if rank == 0:
         line = {
@@ -326,6 +376,8 @@ def run_b200(args, world, rank, local):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "accuracy": acc,
         }
+        if per_k is not None:
+            line["per_k"] = per_k
         print(json.dumps(line), flush=True)
 
 

@@ -130,6 +130,12 @@ int boysfn_generate_uniform(double* d_x, size_t n, uint64_t seed, uint64_t offse
 int boysfn_generate_loguniform(double* d_x, size_t n, uint64_t seed, uint64_t offset,
                                double log10_lo, double log10_hi, void* stream);
 
+/* configs[2] boundary stress: x clustered at 0+, x0 and x1 (+-j ulps with
+ * |j| <= 64, +-10^-s with s ~ U[1,15], or U[b-1, b+1]), |x| taken, every x
+ * keyed by its global index (so warps mix regions). */
+int boysfn_generate_boundary(double* d_x, size_t n, uint64_t seed, uint64_t offset, double x0, double x1,
+                             void* stream);
+
 /* Number of this library's kernels launched by the calling process so far
  * (bench.py reports the delta over its timed region as gpu_launches). */
 unsigned long long boysfn_kernel_launch_count(void);

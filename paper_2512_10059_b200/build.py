@@ -29,8 +29,8 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra"]
 
-CU_SOURCES = ["kernels_soa.cu", "kernels_aos_tma.cu", "kernels_aos_xpose.cu", "kernels_soa_block.cu",
-              "kernels_aos_block.cu", "kernels_soa_binned.cu", "kernels_aos_binned.cu",
+CU_SOURCES = ["kernels_soa.cu", "kernels_aos_xpose.cu", "kernels_soa_block.cu", "kernels_soa_binned.cu",
+              "kernels_aos_binned.cu",
               "kernels_soa_block_tma.cu", "kernels_aos_block_tma.cu", "capi.cu"]
 CPP_SOURCES = ["shim_tables.cpp", "shim_eval.cpp"]
 

@@ -18,10 +18,8 @@ constexpr int kKernelKmax = 32;
 
 // Kernel entry points, one translation unit per store path.
 const void* kernel_soa(int k, int variant);
-const void* kernel_aos_tma(int k, int variant);
 const void* kernel_aos_xpose(int k, int variant);
 const void* kernel_soa_block(int k, int variant);
-const void* kernel_aos_block(int k, int variant);
 const void* kernel_soa_binned(int k, int variant);
 const void* kernel_aos_binned(int k, int variant);
 const void* kernel_soa_block_tma(int k, int variant);

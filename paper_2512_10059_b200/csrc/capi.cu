@@ -212,7 +212,7 @@ bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R, int 
 //   SoA: k <= 6 binned, else block-TMA (block/LSU if no tensor map applies)
 //   AoS: k <= 6 or k == 8 binned; k+1 odd block-TMA; k+1 even transpose
 // BOYSFN_SOA_PATH = warp|block|binned|blocktma and
-// BOYSFN_AOS_PATH = tma|xpose|block|binned|blocktma override the choice
+// BOYSFN_AOS_PATH = xpose|binned|blocktma override the choice
 // (experiments and the path-equivalence tests).
 int choose_store(int layout, int k, const double* d_out) {
   const int R = k + 1;
@@ -226,9 +226,7 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "blocktma") return boysfn_dev::kStoreSoABlockTma;
     return k <= 6 ? boysfn_dev::kStoreSoABinned : boysfn_dev::kStoreSoABlockTma;
   }
-  if (want == "tma" && (R & 1) && a16) return boysfn_dev::kStoreAoSTma;
   if (want == "xpose") return boysfn_dev::kStoreAoSXpose;
-  if (want == "block") return boysfn_dev::kStoreAoSBlock;
   if (want == "binned") return boysfn_dev::kStoreAoSBinned;
   if (want == "blocktma" && a16) return boysfn_dev::kStoreAoSBlockTma;
   if (!want.empty()) return boysfn_dev::kStoreAoSXpose;
@@ -268,20 +266,12 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
     case boysfn_dev::kStoreSoA:
       fn = boysfn_dev::kernel_soa(k, v);
       break;
-    case boysfn_dev::kStoreAoSTma:
-      fn = boysfn_dev::kernel_aos_tma(k, v);
-      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * 32 * R;
-      break;
     case boysfn_dev::kStoreAoSXpose:
       fn = boysfn_dev::kernel_aos_xpose(k, v);
       smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::kXposePitch * R;
       break;
     case boysfn_dev::kStoreSoABlock:
       fn = boysfn_dev::kernel_soa_block(k, v);
-      smem = sizeof(double) * boysfn_dev::kBlockX * R;
-      break;
-    case boysfn_dev::kStoreAoSBlock:
-      fn = boysfn_dev::kernel_aos_block(k, v);
       smem = sizeof(double) * boysfn_dev::kBlockX * R;
       break;
     case boysfn_dev::kStoreSoABinned:
@@ -552,6 +542,38 @@ __global__ void gen_loguniform_kernel(double* x, size_t n, uint64_t seed, uint64
     x[i] = exp10(__dadd_rn(lo, __dmul_rn(span, uniform01(seed, offset + i))));
 }
 
+// configs[2] boundary stress: each x independently
+// picks a breakpoint b in {0+, x0, x1} and a mode -- b +- j ulps (|j| <= 64),
+// b +- 10^-s with s ~ U[1,15], or b + U[-1,1] -- then |.|; keyed by the global
+// index, so consecutive x (one warp) mix regions like a shuffled batch.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void gen_boundary_kernel(double* x, size_t n, uint64_t seed, uint64_t offset, double x0, double x1) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const uint64_t z = mix64(seed + (offset + i + 1) * 0x9E3779B97F4A7C15ull);
+    const uint64_t w = mix64(z ^ 0xD1B54A32D192ED03ull);
+    const int which = static_cast<int>(z % 3), mode = static_cast<int>((z >> 8) % 3);
+    const double u = static_cast<double>(w >> 11) * 0x1.0p-53;
+    const double b = which == 0 ? 0.0 : which == 1 ? x0 : x1;
+    double v;
+    if (mode == 0) {
+      const long long j = static_cast<long long>((w >> 20) % 129) - 64;
+      v = b == 0.0 ? static_cast<double>(j < 0 ? -j : j) * 4.9406564584124654e-324
+                   : __longlong_as_double(__double_as_longlong(b) + j);
+    } else if (mode == 1) {
+      const double off = exp10(-(1.0 + 14.0 * u));
+      v = ((w >> 10) & 1) ? b + off : b - off;
+    } else {
+      v = b + (2.0 * u - 1.0);
+    }
+    x[i] = fabs(v);
+  }
+}
+
 int gen_grid(size_t n, unsigned* grid) {
   int dev = 0, sms = 0;
   CUDA_TRY(cudaGetDevice(&dev));
@@ -582,6 +604,18 @@ BOYSFN_API int boysfn_generate_loguniform(double* d_x, size_t n, uint64_t seed, 
   if (int st = gen_grid(n, &grid)) return st;
   gen_loguniform_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_x, n, seed, offset, log10_lo,
                                                                              log10_hi - log10_lo);
+  CUDA_TRY(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_generate_boundary(double* d_x, size_t n, uint64_t seed, uint64_t offset, double x0,
+                                        double x1, void* stream) {
+  if (n == 0) return BOYSFN_OK;
+  if (d_x == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
+  unsigned grid = 0;
+  if (int st = gen_grid(n, &grid)) return st;
+  gen_boundary_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_x, n, seed, offset, x0, x1);
   CUDA_TRY(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return BOYSFN_OK;

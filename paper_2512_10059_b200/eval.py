@@ -206,5 +206,14 @@ def generate_loguniform(x, seed, log10_lo, log10_hi, offset=0, stream=None):
                                                   log10_hi, ctypes.c_void_p(s.cuda_stream)))
 
 
+def generate_boundary(x, seed, offset=0, tables=None, stream=None):
+    """configs[2] boundary-stress stream around 0+, x0 and x1 (boysfn_b200.h)."""
+    import torch
+    t = tables if tables is not None else embedded_default()
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _raise(_capi.lib().boysfn_generate_boundary(x.data_ptr(), x.numel(), seed, offset, t.x0, t.x1,
+                                                ctypes.c_void_p(s.cuda_stream)))
+
+
 def kernel_launch_count():
     return int(_capi.lib().boysfn_kernel_launch_count())

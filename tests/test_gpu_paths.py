@@ -1,4 +1,4 @@
-"""Every output path (per-warp SoA/AoS-TMA/AoS-transpose, block-tile, and
+"""Every output path (per-warp SoA / AoS-transpose, block-tile LSU and TMA,
 region-binned kernels) computes each value with the same arithmetic routine, so
 all must agree BIT FOR BIT with one another -- on ragged sizes around the 32-x
 tile, 128-x block and 512-x chunk edges and for every order 0..32.  The default
@@ -12,8 +12,8 @@ import paper_2512_10059_b200 as pkg
 
 pytestmark = pytest.mark.gpu
 
-PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("aos", "tma"),
-         ("aos", "xpose"), ("aos", "block"), ("aos", "binned"), ("aos", "blocktma")]
+PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("aos", "xpose"),
+         ("aos", "binned"), ("aos", "blocktma")]
 
 
 def run(torch, x, k, lay, path, monkeypatch):

@@ -96,6 +96,8 @@ def peaks():
 def ncu_traffic(cfg):
     """DRAM bytes per launch from the committed ncu --set full capture, when it
     was taken on this workload (profiles/ncu_summary.json)."""
+    if cfg.get("ks"):
+        return None  # a sweep has no single dominant launch
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)

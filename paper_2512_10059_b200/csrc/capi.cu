@@ -114,7 +114,6 @@ int build_handle(const boysfn_table_desc* d, boysfn_tables_s* h) {
     EvalParams& p = h->params[k];
     p.x0 = d->x0;
     p.x1 = d->x1;
-    p.force_region = -1;
     const bool ok = fill_rational(d->r_A[k], p.numA, p.denA) && fill_rational(d->r_B, p.numB, p.denB);
     h->degree_ok[k] = ok ? 1 : 0;
     int na, ma, nb, mb;
@@ -237,8 +236,7 @@ int choose_store(int layout, int k, const double* d_out) {
 
 // Launches the evaluation kernel; k already validated against the handle.
 int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out,
-                int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad,
-                int force_region) {
+                int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad) {
   if (n == 0) return BOYSFN_OK;
   if (k > boysfn_dev::kKernelKmax)
     return fail(BOYSFN_ERR_UNSUPPORTED, "device kernels evaluate k <= 32");
@@ -290,7 +288,6 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   const size_t want = (ntiles + wpb - 1) / wpb;
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
   EvalParams p = t->params[k];
-  p.force_region = force_region;
   // Per-launch tile counter from the stream-ordered pool: zeroed, used and
   // released in stream order, so concurrent launches on other streams never
   // share it.
@@ -417,7 +414,7 @@ BOYSFN_API int boysfn_eval_device(boysfn_tables_t t, const double* d_x, size_t n
   if (d_x == nullptr || d_out == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
   if (layout == BOYSFN_LAYOUT_SOA && ld < n) return fail(BOYSFN_ERR_ARG, "SOA ld must be >= n");
   return launch_eval(t, d_x, n, k, d_out, layout, ld, static_cast<cudaStream_t>(stream),
-                     d_first_bad, -1);
+                     d_first_bad);
 }
 
 BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, int k, double* out,
@@ -452,7 +449,7 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     const size_t off = c * cx, cn = std::min(cx, n - off);
     CUDA_TRY(cudaMemcpyAsync(P->d_x[s], xs + off, cn * sizeof(double), cudaMemcpyHostToDevice, P->stream[s]));
     CUDA_TRY(cudaMemsetAsync(P->d_bad + s, 0xFF, sizeof(unsigned long long), P->stream[s]));
-    if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], P->d_bad + s, -1))
+    if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], P->d_bad + s))
       return st;
     CUDA_TRY(cudaMemcpyAsync(P->h_bad + s, P->d_bad + s, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              P->stream[s]));
@@ -511,9 +508,12 @@ BOYSFN_API int boysfn_eval_region_host(boysfn_tables_t t, double x, int k, int r
   if (int st = get_pipeline(&P)) return st;
   cudaStream_t s = P->stream[0];
   CUDA_TRY(cudaStreamSynchronize(s));
-  CUDA_TRY(cudaMemcpyAsync(P->d_x[0], &x, sizeof(double), cudaMemcpyHostToDevice, s));
-  if (int st = launch_eval(t, P->d_x[0], 1, k, P->d_out[0], BOYSFN_LAYOUT_AOS, 1, s, nullptr, region))
-    return st;
+  if (k > boysfn_dev::kKernelKmax) return fail(BOYSFN_ERR_UNSUPPORTED, "device kernels evaluate k <= 32");
+  if (!t->degree_ok[k]) return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
+  EvalParams p = t->params[k];
+  void* args[] = {&p, &x, &region, &P->d_out[0]};
+  CUDA_TRY(cudaLaunchKernel(boysfn_dev::kernel_region(k, t->variant[k]), dim3(1), dim3(1), args, 0, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   CUDA_TRY(cudaMemcpyAsync(out, P->d_out[0], (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return BOYSFN_OK;

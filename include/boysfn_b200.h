@@ -119,6 +119,15 @@ int boysfn_eval_host(boysfn_tables_t tables, const double* xs, size_t n, int k, 
  * reference's branch-agreement test seam), computed on the device. */
 int boysfn_eval_region_host(boysfn_tables_t tables, double x, int k, int region, double* out);
 
+/* Algorithm 2 of the paper, fused on the
+ * device: z_i = sum_{l=0..k} c_l sum_j F_l(x_i + x_j) y_j for i < n, with
+ * x, y, z device arrays of n doubles (x >= 0, finite), c a HOST array of k+1
+ * doubles.  F_l are Algorithm 1's values (regions A/B/C of the table set);
+ * no Boys value is stored.  Enqueued on `stream` (sort, gather, O(n^2) pair
+ * kernel, scatter), asynchronous; scratch comes from the stream-ordered pool. */
+int boysfn_alg2_device(boysfn_tables_t tables, const double* d_x, const double* d_y, size_t n, int k,
+                       const double* c, double* d_z, void* stream);
+
 /* Synthetic workload: x[i] = lo + (hi-lo)*u_i with u_i = (splitmix64(seed +
  * (offset+i+1)*0x9E3779B97F4A7C15) >> 11) * 2^-53, the multiply and add
  * separately rounded, so any CPU restating the formula reproduces it bit for

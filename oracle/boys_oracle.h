@@ -53,6 +53,9 @@ int oracle_boys_batch_many_mt(const double* xs, size_t n, int k, const oracle_ta
                               double* out, int nthreads);
 void oracle_gen_uniform(double* x, size_t n, uint64_t seed, uint64_t offset, double lo,
                         double hi);
+/* Algorithm 2 by direct summation. */
+int oracle_alg2_direct(const double* x, const double* y, size_t n, int k, const double* c,
+                       const oracle_tables* t, double* z, double* zabs, int nthreads);
 
 /* ---- extended-precision oracle (boys_hp.c) ---- */
 /* F_0..F_kmax at x, rounded to double (verify.cpp:38 convention). */

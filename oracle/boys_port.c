@@ -154,6 +154,64 @@ int oracle_boys_batch_many_mt(const double* xs, size_t n, int k, const oracle_ta
   return st;
 }
 
+/* ---- Algorithm 2 direct summation (the benchmark's correctness
+ * oracle): z_i = sum_j y_j sum_l c_l F_l(x_i + x_j) with every F from the
+ * reference restatement above; zabs_i = sum_j |y_j sum_l c_l F_l| scales the
+ * relative tolerance.  Rows are split over threads. */
+typedef struct {
+  const double *x, *y, *c;
+  size_t n, i0, i1;
+  int k;
+  const oracle_tables* t;
+  double *z, *zabs;
+  int status;
+} alg2_job;
+
+static void* alg2_worker(void* arg) {
+  alg2_job* j = (alg2_job*)arg;
+  double F[130];
+  for (size_t i = j->i0; i < j->i1; ++i) {
+    double z = 0, za = 0;
+    for (size_t jj = 0; jj < j->n; ++jj) {
+      if (oracle_boys_batch(j->x[i] + j->x[jj], j->k, j->t, F) != ORACLE_OK) {
+        j->status = ORACLE_ERR_DOMAIN;
+        return NULL;
+      }
+      double w = 0;
+      for (int l = 0; l <= j->k; ++l) w += j->c[l] * F[l];
+      z += j->y[jj] * w;
+      za += fabs(j->y[jj] * w);
+    }
+    j->z[i] = z;
+    if (j->zabs) j->zabs[i] = za;
+  }
+  return NULL;
+}
+
+int oracle_alg2_direct(const double* x, const double* y, size_t n, int k, const double* c,
+                       const oracle_tables* t, double* z, double* zabs, int nthreads) {
+  if (k < 0 || k > t->k_max || k >= 130) return ORACLE_ERR_RANGE;
+  if (nthreads < 1) nthreads = 1;
+  if ((size_t)nthreads > n) nthreads = n ? (int)n : 1;
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  alg2_job* jobs = (alg2_job*)calloc((size_t)nthreads, sizeof(alg2_job));
+  size_t begin = 0;
+  for (int w = 0; w < nthreads; ++w) {
+    const size_t cnt = n / nthreads + ((size_t)w < n % nthreads ? 1 : 0);
+    jobs[w] = (alg2_job){x, y, c, n, begin, begin + cnt, k, t, z, zabs, 0};
+    pthread_create(&th[w], NULL, alg2_worker, &jobs[w]);
+    begin += cnt;
+  }
+  int st = ORACLE_OK;
+  for (int w = 0; w < nthreads; ++w) {
+    pthread_join(th[w], NULL);
+    if (jobs[w].status != ORACLE_OK) st = jobs[w].status;
+  }
+  free(th);
+  free(jobs);
+  return st;
+}
+
 /* ---- synthetic workload generator shared with the device generator
  * (paper_2512_10059_b200/csrc/boys_kernels.cu: gen_uniform_kernel).  splitmix64
  * keyed by the global index, so shards of any size reproduce one stream. */

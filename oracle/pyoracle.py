@@ -71,6 +71,8 @@ class Port:
         L.oracle_classify_region.argtypes = [ctypes.c_double, ctypes.POINTER(_Tables)]
         L.oracle_gen_uniform.argtypes = [_dp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_double, ctypes.c_double]
+        L.oracle_alg2_direct.argtypes = [_dp, _dp, ctypes.c_size_t, ctypes.c_int, _dp, ctypes.POINTER(_Tables), _dp,
+                                         _dp, ctypes.c_int]
         L.oracle_hp_boys_batch_many.argtypes = [ctypes.c_int, _dp, ctypes.c_size_t, _dp, ctypes.c_int]
         L.oracle_hp_boys_batch.argtypes = [ctypes.c_int, ctypes.c_double, _dp]
         L.oracle_hp_series.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int]
@@ -127,6 +129,17 @@ class Port:
         x = np.empty(n, dtype=np.float64)
         self.L.oracle_gen_uniform(x.ctypes.data_as(_dp), n, seed, offset, lo, hi)
         return x
+
+    def alg2(self, x, y, c, threads=None):
+        """Algorithm 2 by direct summation: (z, sum_j |y_j w_ij|)."""
+        x, y, c = (np.ascontiguousarray(a, dtype=np.float64) for a in (x, y, c))
+        z, za = np.zeros(x.size), np.zeros(x.size)
+        st = self.L.oracle_alg2_direct(x.ctypes.data_as(_dp), y.ctypes.data_as(_dp), x.size, c.size - 1,
+                                       c.ctypes.data_as(_dp), ctypes.byref(self.tables), z.ctypes.data_as(_dp),
+                                       za.ctypes.data_as(_dp), threads or os.cpu_count() or 1)
+        if st:
+            raise RuntimeError("alg2 oracle status %d" % st)
+        return z, za
 
     def hp(self, xs, kmax, threads=None):
         """Extended-precision F_0..F_kmax rounded to double, shape (N, kmax+1)."""

@@ -8,13 +8,13 @@ FP64 kernels (csrc/); see DESIGN.md.
 """
 from .tables import (CoefficientTableSet, RationalApproximant, TableParseError, embedded_default,
                      emit_tables, parse_tables, validate_tables)
-from .eval import (BoysBatch, DeviceTables, Region, boys_batch, boys_batch_many, boys_batch_region,
+from .eval import (BoysBatch, alg2, DeviceTables, Region, boys_batch, boys_batch_many, boys_batch_region,
                    classify_region, cuda_error, domain_error, eval_device, generate_boundary, generate_loguniform,
                    generate_uniform, invalid_argument, kernel_launch_count, out_of_range, unsupported)
 
 __all__ = [
     "CoefficientTableSet", "RationalApproximant", "TableParseError", "embedded_default", "emit_tables",
-    "parse_tables", "validate_tables", "BoysBatch", "DeviceTables", "Region", "boys_batch",
+    "parse_tables", "validate_tables", "alg2", "BoysBatch", "DeviceTables", "Region", "boys_batch",
     "boys_batch_many", "boys_batch_region", "classify_region", "cuda_error", "domain_error",
     "eval_device", "generate_boundary", "generate_loguniform", "generate_uniform", "invalid_argument",
     "kernel_launch_count", "out_of_range", "unsupported",

@@ -58,6 +58,9 @@ _SIGNATURES = [
     ("boysfn_generate_boundary", ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64,
                                                 ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                                 ctypes.c_void_p]),
+    ("boysfn_alg2_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                          ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p,
+                                          ctypes.c_void_p]),
     ("boysfn_kernel_launch_count", ctypes.c_ulonglong, []),
 ]
 

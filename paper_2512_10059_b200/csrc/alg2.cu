@@ -1,0 +1,109 @@
+// alg2.cu -- C ABI of Algorithm 2 (the paper's fused Boys benchmark,
+// PAPER.md:353-390) and its kernel instantiations:
+//     z_i = sum_{l=0..k} c_l sum_j F_l(x_i + x_j) y_j.
+// Pipeline (one stream, stream-ordered scratch): CUB radix sort of x with the
+// original index -> gather (x, e^{-x}, y) in sorted order -> the fused pair
+// kernel (alg2_device.cuh) -> scatter z back to the caller's order.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <utility>
+
+#include "alg2_device.cuh"
+#include "boys_launch.h"
+#include "capi_internal.h"
+#include "embedded_tables.inc"
+
+namespace boysfn_dev {
+namespace {
+
+template <int K, int V>
+const void* alg2_entry() {
+  constexpr int NA = V == kVariantEmbedded ? kEmbDegA[K][0] : kMaxCoef - 1;
+  constexpr int MA = V == kVariantEmbedded ? kEmbDegA[K][1] : kMaxCoef - 1;
+  constexpr int NB = V == kVariantEmbedded ? kEmbDegB[0] : kMaxCoef - 1;
+  constexpr int MB = V == kVariantEmbedded ? kEmbDegB[1] : kMaxCoef - 1;
+  return reinterpret_cast<const void*>(&boys_alg2_kernel<K, NA, MA, NB, MB>);
+}
+
+template <size_t... Ks>
+const void* alg2_lookup(int k, int v, std::index_sequence<Ks...>) {
+  static const void* const table[2][sizeof...(Ks)] = {
+      {alg2_entry<static_cast<int>(Ks), kVariantEmbedded>()...},
+      {alg2_entry<static_cast<int>(Ks), kVariantPadded>()...}};
+  return table[v][k];
+}
+
+__global__ void iota_kernel(unsigned* idx, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    idx[i] = static_cast<unsigned>(i);
+}
+
+__global__ void gather_kernel(const unsigned* perm, const double* xs_sorted, const double* y, double* es,
+                              double* ys, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    es[i] = exp(-xs_sorted[i]);
+    ys[i] = y[perm[i]];
+  }
+}
+
+__global__ void scatter_kernel(const unsigned* perm, const double* zs, double* z, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    z[perm[i]] = zs[i];
+}
+
+}  // namespace
+}  // namespace boysfn_dev
+
+BOYSFN_API int boysfn_alg2_device(boysfn_tables_t t, const double* d_x, const double* d_y, size_t n, int k,
+                                  const double* c, double* d_z, void* stream_) {
+  using namespace boysfn_dev;
+  using boysfn_internal::fail;
+  if (t == nullptr || c == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
+  if (k < 0 || k > t->k_max) return fail(BOYSFN_ERR_RANGE, "boys_batch: k out of range for this table set");
+  if (k > kKernelKmax) return fail(BOYSFN_ERR_UNSUPPORTED, "device kernels evaluate k <= 32");
+  if (!t->degree_ok[k]) return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
+  if (n == 0) return BOYSFN_OK;
+  if (n >= (size_t(1) << 32)) return fail(BOYSFN_ERR_UNSUPPORTED, "Algorithm 2 takes n < 2^32");
+  if (d_x == nullptr || d_y == nullptr || d_z == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  int dev = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid1 = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, size_t(sms) * 8));
+
+  // scratch: sorted x, e, y, z (doubles), index in/out (u32), CUB temp
+  size_t cub_bytes = 0;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, static_cast<const double*>(nullptr),
+                                           static_cast<double*>(nullptr), static_cast<const unsigned*>(nullptr),
+                                           static_cast<unsigned*>(nullptr), n, 0, 64, s));
+  const size_t dbl = ((n * sizeof(double) + 255) / 256) * 256, u32 = ((n * sizeof(unsigned) + 255) / 256) * 256;
+  char* scratch = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), 4 * dbl + 2 * u32 + cub_bytes, s));
+  double* xs = reinterpret_cast<double*>(scratch);
+  double* es = reinterpret_cast<double*>(scratch + dbl);
+  double* ys = reinterpret_cast<double*>(scratch + 2 * dbl);
+  double* zs = reinterpret_cast<double*>(scratch + 3 * dbl);
+  unsigned* idx = reinterpret_cast<unsigned*>(scratch + 4 * dbl);
+  unsigned* perm = reinterpret_cast<unsigned*>(scratch + 4 * dbl + u32);
+  void* cub_tmp = scratch + 4 * dbl + 2 * u32;
+
+  int status = BOYSFN_OK;
+  iota_kernel<<<grid1, 256, 0, s>>>(idx, n);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, d_x, xs, idx, perm, n, 0, 64, s);
+  if (e == cudaSuccess) {
+    gather_kernel<<<grid1, 256, 0, s>>>(perm, xs, d_y, es, ys, n);
+    Alg2Coef coef{};
+    for (int l = 0; l <= k; ++l) coef.c[l] = c[l];
+    EvalParams p = t->params[k];
+    void* args[] = {&p, &coef, &xs, &es, &ys, &n, &zs};
+    const unsigned grid2 = static_cast<unsigned>((n + kAlg2Threads - 1) / kAlg2Threads);
+    e = cudaLaunchKernel(alg2_lookup(k, t->variant[k], std::make_index_sequence<kKernelKmax + 1>{}), dim3(grid2),
+                         dim3(kAlg2Threads), args, 0, s);
+    if (e == cudaSuccess) scatter_kernel<<<grid1, 256, 0, s>>>(perm, zs, d_z, n);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) status = boysfn_internal::cuda_fail(e, "boysfn_alg2_device");
+  cudaFreeAsync(scratch, s);
+  for (int i = 0; i < 4; ++i) boysfn_internal::count_launch();  // iota, gather, pairs, scatter (CUB's sort not counted)
+  return status;
+}

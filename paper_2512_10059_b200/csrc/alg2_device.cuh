@@ -1,0 +1,106 @@
+// alg2_device.cuh -- Algorithm 2 of arXiv 2512.10059 (PAPER.md:353-390,
+// SPEC.md:494-502): the fused Boys-and-contraction benchmark
+//     z_i = sum_{l=0..k} c_l sum_j F_l(x_i + x_j) y_j
+// evaluated on the B200 without storing a single Boys value.
+//
+// The O(N^2) pair sweep is FP64-bound, so the design goal is zero wasted FP64
+// work:
+//   * x is sorted once (CUB radix sort, with y carried along); a warp then
+//     holds 32 neighbouring x_i, and for one x_j the 32 sums x_i + x_j almost
+//     always fall in the same region -- the A/B/C branches are warp-uniform
+//     without any per-pair binning;
+//   * blocks stage tiles of (x_j, e^{-x_j}, y_j) in shared memory (broadcast
+//     reads); each thread owns one x_i and accumulates z_i in a register;
+//   * per pair, F_0..F_k are produced by the same recurrences as the bulk kernel
+//     (boys_device.cuh) but folded into w = sum_l c_l F_l on the fly, so F never
+//     exists as an array; e^{-(x_i+x_j)} = e^{-x_i} e^{-x_j} replaces one exp
+//     per pair by one multiply (<= 1.5 ulp instead of <= 1 ulp on e; the
+//     benchmark's contract is agreement with the direct sum within N k 1e-12
+//     relative).
+#pragma once
+
+#include "boys_device.cuh"
+
+namespace boysfn_dev {
+
+constexpr int kAlg2Threads = 128;  // x_i per block
+constexpr int kAlg2TileJ = 256;    // x_j per shared-memory tile
+
+struct Alg2Coef {
+  double c[kMaxCoef + 16];  // c_0..c_k, k <= 32
+};
+
+#ifdef __CUDACC__
+
+// w = sum_l c_l F_l(s) for one argument s, given e = e^{-s}.
+template <int K, int NA, int MA, int NB, int MB>
+__device__ __forceinline__ double boys_dot(const EvalParams& P, const Alg2Coef& C, double s, double e) {
+  if (s < P.x0) {  // region A: seed F_K, downward (eval.cpp:38-47)
+    double F = rational<NA, MA>(P.numA, P.denA, s);
+    double w = C.c[K] * F;
+    const double twos = s + s;
+#pragma unroll
+    for (int l = K - 1; l >= 0; --l) {
+      const double t = __fma_rn(twos, F, e);
+      F = (l == 0) ? t : __dmul_rn(t, recip_odd(l));
+      w = __fma_rn(C.c[l], F, w);
+    }
+    return w;
+  }
+  // regions B and C: seed F_0, upward (eval.cpp:49-57, 73-77)
+  const double inv2s = __ddiv_rn(0.5, s);
+  double F, tail;
+  if (s < P.x1) {
+    F = rational<NB, MB>(P.numB, P.denB, s);
+    tail = -__dmul_rn(e, inv2s);
+  } else {
+    F = __ddiv_rn(kHalfSqrtPi, __dsqrt_rn(s));
+    tail = -0.0;
+  }
+  double w = C.c[0] * F;
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+    F = __fma_rn(__dmul_rn(static_cast<double>(2 * l + 1), inv2s), F, tail);
+    w = __fma_rn(C.c[l + 1], F, w);
+  }
+  return w;
+}
+
+// One thread per (sorted) x_i; all x_j streamed through shared memory.
+// xs sorted ascending, es = e^{-xs}, ys carried along; zs in sorted order.
+template <int K, int NA, int MA, int NB, int MB>
+__global__ void __launch_bounds__(kAlg2Threads)
+    boys_alg2_kernel(const __grid_constant__ EvalParams P, const __grid_constant__ Alg2Coef C,
+                     const double* __restrict__ xs, const double* __restrict__ es,
+                     const double* __restrict__ ys, size_t n, double* __restrict__ zs) {
+  __shared__ double sx[kAlg2TileJ], se[kAlg2TileJ], sy[kAlg2TileJ];
+  const int tid = threadIdx.x;
+  const size_t i = static_cast<size_t>(blockIdx.x) * kAlg2Threads + tid;
+  const double xi = i < n ? xs[i] : 0.0;
+  const double ei = i < n ? es[i] : 1.0;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (size_t j0 = 0; j0 < n; j0 += kAlg2TileJ) {
+#pragma unroll
+    for (int r = 0; r < kAlg2TileJ / kAlg2Threads; ++r) {
+      const size_t j = j0 + r * kAlg2Threads + tid;
+      const bool ok = j < n;
+      sx[r * kAlg2Threads + tid] = ok ? xs[j] : 0.0;
+      se[r * kAlg2Threads + tid] = ok ? es[j] : 1.0;
+      sy[r * kAlg2Threads + tid] = ok ? ys[j] : 0.0;  // padding contributes y = 0
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int jj = 0; jj < kAlg2TileJ; jj += 2) {  // two independent pair chains per step
+      const double w0 = boys_dot<K, NA, MA, NB, MB>(P, C, xi + sx[jj], __dmul_rn(ei, se[jj]));
+      const double w1 = boys_dot<K, NA, MA, NB, MB>(P, C, xi + sx[jj + 1], __dmul_rn(ei, se[jj + 1]));
+      acc0 = __fma_rn(sy[jj], w0, acc0);
+      acc1 = __fma_rn(sy[jj + 1], w1, acc1);
+    }
+    __syncthreads();
+  }
+  if (i < n) zs[i] = acc0 + acc1;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace boysfn_dev

@@ -18,9 +18,8 @@
 
 #include "../../include/boysfn_b200.h"
 #include "boys_launch.h"
+#include "capi_internal.h"
 #include "embedded_tables.inc"
-
-#define BOYSFN_API extern "C" __attribute__((visibility("default")))
 
 using boysfn_dev::EvalParams;
 using boysfn_dev::kMaxCoef;
@@ -35,36 +34,24 @@ constexpr const char* kMsgRange = "boys_batch: k out of range for this table set
 constexpr const char* kMsgUpward = "upward_recursion: x must be positive";
 
 thread_local std::string t_last_error;
-
-int fail(int status, const std::string& msg) {
-  t_last_error = msg;
-  return status;
-}
-
-int cuda_fail(cudaError_t e, const char* where) {
-  t_last_error = std::string(where) + ": " + cudaGetErrorString(e);
-  return BOYSFN_ERR_CUDA;
-}
-
-#define CUDA_TRY(call)                                   \
-  do {                                                   \
-    cudaError_t e_ = (call);                             \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
-  } while (0)
-
 std::atomic<unsigned long long> g_launches{0};
 
 }  // namespace
 
-// ------------------------------------------------------------ table image --
-struct boysfn_tables_s {
-  double x0 = 0, x1 = 0, eps_tol = 0;
-  int k_max = 0;
-  bool is_embedded = false;
-  std::vector<EvalParams> params;  // one launch image per order k <= device kmax
-  std::vector<int> variant;        // kernel degree variant per k
-  std::vector<int> degree_ok;      // 1 if r_A[k], r_B fit the device image
-};
+int boysfn_internal::fail(int status, const std::string& msg) {
+  t_last_error = msg;
+  return status;
+}
+
+int boysfn_internal::cuda_fail(cudaError_t e, const char* where) {
+  t_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return BOYSFN_ERR_CUDA;
+}
+
+void boysfn_internal::count_launch() { boysfn_internal::count_launch(); }
+
+using boysfn_internal::cuda_fail;
+using boysfn_internal::fail;
 
 namespace {
 
@@ -298,7 +285,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
   CUDA_TRY(cudaFreeAsync(counter, stream));
   if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  boysfn_internal::count_launch();
   return BOYSFN_OK;
 }
 
@@ -513,7 +500,7 @@ BOYSFN_API int boysfn_eval_region_host(boysfn_tables_t t, double x, int k, int r
   EvalParams p = t->params[k];
   void* args[] = {&p, &x, &region, &P->d_out[0]};
   CUDA_TRY(cudaLaunchKernel(boysfn_dev::kernel_region(k, t->variant[k]), dim3(1), dim3(1), args, 0, s));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  boysfn_internal::count_launch();
   CUDA_TRY(cudaMemcpyAsync(out, P->d_out[0], (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return BOYSFN_OK;
@@ -592,7 +579,7 @@ BOYSFN_API int boysfn_generate_uniform(double* d_x, size_t n, uint64_t seed, uin
   if (int st = gen_grid(n, &grid)) return st;
   gen_uniform_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_x, n, seed, offset, lo, hi - lo);
   CUDA_TRY(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  boysfn_internal::count_launch();
   return BOYSFN_OK;
 }
 
@@ -605,7 +592,7 @@ BOYSFN_API int boysfn_generate_loguniform(double* d_x, size_t n, uint64_t seed, 
   gen_loguniform_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_x, n, seed, offset, log10_lo,
                                                                              log10_hi - log10_lo);
   CUDA_TRY(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  boysfn_internal::count_launch();
   return BOYSFN_OK;
 }
 
@@ -617,7 +604,7 @@ BOYSFN_API int boysfn_generate_boundary(double* d_x, size_t n, uint64_t seed, ui
   if (int st = gen_grid(n, &grid)) return st;
   gen_boundary_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_x, n, seed, offset, x0, x1);
   CUDA_TRY(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  boysfn_internal::count_launch();
   return BOYSFN_OK;
 }
 

@@ -215,5 +215,22 @@ def generate_boundary(x, seed, offset=0, tables=None, stream=None):
                                                 ctypes.c_void_p(s.cuda_stream)))
 
 
+def alg2(x, y, c, k=None, z=None, tables=None, stream=None):
+    """Algorithm 2: z_i = sum_l c_l sum_j F_l(x_i + x_j) y_j on
+    the device.  x, y: CUDA float64 tensors of n; c: k+1 host floats; returns
+    z (a new CUDA tensor unless given).  Asynchronous on `stream`."""
+    import torch
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    k = len(c) - 1 if k is None else int(k)
+    if z is None:
+        z = torch.empty_like(x)
+    tables = tables if tables is not None else embedded_default()
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _raise(_capi.lib().boysfn_alg2_device(_handle(tables).handle, x.data_ptr(), y.data_ptr(), x.numel(), k,
+                                          c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), z.data_ptr(),
+                                          ctypes.c_void_p(s.cuda_stream)))
+    return z
+
+
 def kernel_launch_count():
     return int(_capi.lib().boysfn_kernel_launch_count())

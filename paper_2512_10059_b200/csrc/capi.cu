@@ -48,7 +48,7 @@ int boysfn_internal::cuda_fail(cudaError_t e, const char* where) {
   return BOYSFN_ERR_CUDA;
 }
 
-void boysfn_internal::count_launch() { boysfn_internal::count_launch(); }
+void boysfn_internal::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 using boysfn_internal::cuda_fail;
 using boysfn_internal::fail;

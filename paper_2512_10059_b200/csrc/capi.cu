@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -14,6 +16,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/boysfn_b200.h"
@@ -297,19 +300,23 @@ struct Pipeline {
   static constexpr size_t kChunkOutBytes = size_t(128) << 20;
   int device = -1;
   cudaStream_t stream[kSlots] = {};
-  cudaEvent_t done[kSlots] = {};
+  cudaEvent_t done[kSlots] = {};    // kernel + first-bad flag of the slot's chunk
+  cudaEvent_t copied[kSlots] = {};  // D2H of the slot's chunk
   double* d_x[kSlots] = {};
   double* d_out[kSlots] = {};
   unsigned long long* d_bad = nullptr;  // kSlots words
   unsigned long long* h_bad = nullptr;  // pinned, kSlots words
   size_t cap_x = 0;                     // x capacity per slot
   size_t cap_out = 0;                   // doubles per slot
+  double* h_x[kSlots] = {};             // pinned staging for pageable callers (lazy)
+  double* h_out[kSlots] = {};
 
   int init(int dev) {
     device = dev;
     for (int s = 0; s < kSlots; ++s) {
       CUDA_TRY(cudaStreamCreateWithFlags(&stream[s], cudaStreamNonBlocking));
       CUDA_TRY(cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&copied[s], cudaEventDisableTiming));
     }
     CUDA_TRY(cudaMalloc(&d_bad, kSlots * sizeof(unsigned long long)));
     CUDA_TRY(cudaHostAlloc(&h_bad, kSlots * sizeof(unsigned long long), cudaHostAllocDefault));
@@ -321,7 +328,55 @@ struct Pipeline {
     }
     return BOYSFN_OK;
   }
+
+  int ensure_staging() {
+    for (int s = 0; s < kSlots; ++s) {
+      if (h_x[s] == nullptr) CUDA_TRY(cudaHostAlloc(&h_x[s], cap_x * sizeof(double), cudaHostAllocDefault));
+      if (h_out[s] == nullptr) CUDA_TRY(cudaHostAlloc(&h_out[s], cap_out * sizeof(double), cudaHostAllocDefault));
+    }
+    return BOYSFN_OK;
+  }
 };
+
+// Page-locked (or registered) host memory can be DMA'd directly; pageable
+// memory goes through the pipeline's pinned staging instead of the driver's
+// single-threaded internal staging (which ran at 10-18 GB/s on the B200 hosts).
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// Host-side copy of staged rows to the caller's pageable buffer, split over
+// up to 16 threads (host memcpy: ~15 GB/s on 1 core, 59 on 8, 75 on 16 on the
+// B200 hosts, tools/probe_hostmem.py; PCIe delivers ~55 GB/s).
+struct Segment {
+  double* dst;
+  const double* src;
+  size_t n;
+};
+
+void parallel_copy(std::vector<Segment> segs) {
+  size_t total = 0;
+  for (const auto& g : segs) total += g.n;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int T = static_cast<int>(std::min<size_t>({16, hw, std::max<size_t>(1, total / (1u << 18))}));
+  // cut the segments into pieces of about total/T doubles
+  std::vector<Segment> pieces;
+  const size_t piece = std::max<size_t>(1, (total + T - 1) / T);
+  for (const auto& g : segs)
+    for (size_t o = 0; o < g.n; o += piece) pieces.push_back({g.dst + o, g.src + o, std::min(piece, g.n - o)});
+  auto work = [&](int t) {
+    for (size_t i = t; i < pieces.size(); i += T) std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].n * sizeof(double));
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+}
 
 int get_pipeline(Pipeline** out) {
   thread_local std::map<int, std::unique_ptr<Pipeline>> pipes;
@@ -430,11 +485,21 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
   const size_t cx = std::max<size_t>(32, std::min(P->cap_x, P->cap_out / row) / 32 * 32);
   const size_t nchunks = (n + cx - 1) / cx;
   const int S = Pipeline::kSlots;
+  const bool x_direct = is_pinned(xs) && is_pinned(xs + n - 1);
+  const bool out_direct = is_pinned(out) && is_pinned(out + out_len - 1);
+  if (!(x_direct && out_direct))
+    if (int st = P->ensure_staging()) return st;
 
+  // Chunk c in slot s = c % S: (stage x) -> H2D -> kernel -> first-bad flag.
   auto issue = [&](size_t c) -> int {
     const int s = static_cast<int>(c % S);
     const size_t off = c * cx, cn = std::min(cx, n - off);
-    CUDA_TRY(cudaMemcpyAsync(P->d_x[s], xs + off, cn * sizeof(double), cudaMemcpyHostToDevice, P->stream[s]));
+    const double* src = xs + off;
+    if (!x_direct) {
+      std::memcpy(P->h_x[s], src, cn * sizeof(double));
+      src = P->h_x[s];
+    }
+    CUDA_TRY(cudaMemcpyAsync(P->d_x[s], src, cn * sizeof(double), cudaMemcpyHostToDevice, P->stream[s]));
     CUDA_TRY(cudaMemsetAsync(P->d_bad + s, 0xFF, sizeof(unsigned long long), P->stream[s]));
     if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], P->d_bad + s))
       return st;
@@ -443,15 +508,55 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     CUDA_TRY(cudaEventRecord(P->done[s], P->stream[s]));
     return BOYSFN_OK;
   };
-  auto drain = [&]() {
-    for (int s = 0; s < S; ++s) cudaStreamSynchronize(P->stream[s]);
+  // D2H of the chunk's first `rows` rows: to the caller directly, or to staging.
+  auto fetch = [&](size_t c, size_t rows) -> int {
+    const int s = static_cast<int>(c % S);
+    const size_t off = c * cx, cn = std::min(cx, n - off);
+    if (rows > 0) {
+      if (layout == BOYSFN_LAYOUT_AOS) {
+        double* dst = out_direct ? out + off * row : P->h_out[s];
+        CUDA_TRY(cudaMemcpyAsync(dst, P->d_out[s], rows * row * sizeof(double), cudaMemcpyDeviceToHost,
+                                 P->stream[s]));
+      } else if (out_direct) {
+        CUDA_TRY(cudaMemcpy2DAsync(out + off, ld * sizeof(double), P->d_out[s], cn * sizeof(double),
+                                   rows * sizeof(double), row, cudaMemcpyDeviceToHost, P->stream[s]));
+      } else {
+        CUDA_TRY(cudaMemcpyAsync(P->h_out[s], P->d_out[s], row * cn * sizeof(double), cudaMemcpyDeviceToHost,
+                                 P->stream[s]));
+      }
+    }
+    CUDA_TRY(cudaEventRecord(P->copied[s], P->stream[s]));
+    return BOYSFN_OK;
+  };
+  // Staged path: staging -> caller's pageable rows, on host threads.
+  auto unstage = [&](size_t c, size_t rows) -> int {
+    const int s = static_cast<int>(c % S);
+    const size_t off = c * cx, cn = std::min(cx, n - off);
+    CUDA_TRY(cudaEventSynchronize(P->copied[s]));
+    if (rows == 0) return BOYSFN_OK;
+    std::vector<Segment> segs;
+    if (layout == BOYSFN_LAYOUT_AOS)
+      segs.push_back({out + off * row, P->h_out[s], rows * row});
+    else
+      for (size_t l = 0; l < row; ++l) segs.push_back({out + l * ld + off, P->h_out[s] + l * cn, rows});
+    parallel_copy(std::move(segs));
+    return BOYSFN_OK;
   };
 
+  const bool trace = std::getenv("BOYSFN_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what, size_t c) {
+    if (trace)
+      std::fprintf(stderr, "[eval_host] %8.3f ms %s %zu\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what, c);
+  };
   int status = BOYSFN_OK;
-  for (size_t c = 0; c < std::min<size_t>(nchunks, S - 1); ++c)
-    if ((status = issue(c))) break;
+  size_t pend_c = 0, pend_rows = 0;
+  bool pending = false;  // a staged chunk whose rows still have to reach the caller
+  for (size_t c = 0; c < std::min<size_t>(nchunks, S - 1) && status == BOYSFN_OK; ++c) status = issue(c);
   for (size_t c = 0; c < nchunks && status == BOYSFN_OK; ++c) {
     if (c + S - 1 < nchunks && (status = issue(c + S - 1))) break;
+    stamp("issued", c + S - 1);
     const int s = static_cast<int>(c % S);
     const size_t off = c * cx, cn = std::min(cx, n - off);
     if (cudaError_t e = cudaEventSynchronize(P->done[s])) {
@@ -460,25 +565,23 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     }
     const unsigned long long bad = P->h_bad[s];
     const size_t rows = bad == ~0ull ? cn : static_cast<size_t>(bad);
-    if (rows > 0) {
-      cudaError_t e;
-      if (layout == BOYSFN_LAYOUT_AOS)
-        e = cudaMemcpyAsync(out + off * row, P->d_out[s], rows * row * sizeof(double),
-                            cudaMemcpyDeviceToHost, P->stream[s]);
-      else
-        e = cudaMemcpy2DAsync(out + off, ld * sizeof(double), P->d_out[s], cn * sizeof(double),
-                              rows * sizeof(double), row, cudaMemcpyDeviceToHost, P->stream[s]);
-      if (e != cudaSuccess) {
-        status = cuda_fail(e, "cudaMemcpyAsync D2H");
-        break;
-      }
-    }
+    stamp("kernel done", c);
+    if ((status = fetch(c, rows))) break;
+    if (pending && (status = unstage(pend_c, pend_rows))) break;  // overlaps the D2H of chunk c
+    stamp("unstaged", pend_c);
+    pending = !out_direct;
+    pend_c = c;
+    pend_rows = rows;
     if (bad != ~0ull) {
       if (first_bad) *first_bad = off + static_cast<size_t>(bad);
       status = fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
     }
   }
-  drain();
+  if (pending && (status == BOYSFN_OK || status == BOYSFN_ERR_DOMAIN)) {
+    const int st = unstage(pend_c, pend_rows);
+    if (status == BOYSFN_OK) status = st;
+  }
+  for (int s = 0; s < S; ++s) cudaStreamSynchronize(P->stream[s]);
   if (status == BOYSFN_OK) {
     if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "boysfn_eval_host");
   }

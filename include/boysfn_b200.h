@@ -37,7 +37,7 @@ typedef enum boysfn_status {
   BOYSFN_ERR_TABLES = 4,      /* std::invalid_argument from validate_tables, tables.cpp:14-32 */
   BOYSFN_ERR_CUDA = 5,        /* a CUDA runtime error (no reference equivalent)   */
   BOYSFN_ERR_ARG = 6,         /* NULL handle/pointer or bad layout/ld             */
-  BOYSFN_ERR_UNSUPPORTED = 7  /* k > 32 or a table degree beyond the device image */
+  BOYSFN_ERR_UNSUPPORTED = 7  /* a table degree beyond the device image (or Algorithm 2 with k > 32) */
 } boysfn_status;
 
 /* Output layout.  AOS is the reference's row-major out[i*(k+1)+l]
@@ -69,7 +69,9 @@ typedef struct boysfn_table_desc {
 /* Opaque immutable device-side table image built from a table set. */
 typedef struct boysfn_tables_s* boysfn_tables_t;
 
-/* Largest order the device kernels evaluate (templated unrolled chains). */
+/* Largest order of the templated (unrolled, tuned) kernels; orders above it
+ * -- table sets with k_max > 32, e.g. from the reference's gen path
+ * (k_max <= 64) -- run on the run-time-k generic kernel. */
 #define BOYSFN_DEVICE_KMAX 32
 /* Largest numerator / denominator degree the device image holds. */
 #define BOYSFN_DEVICE_MAX_DEGREE 23

@@ -25,6 +25,7 @@ const void* kernel_aos_binned(int k, int variant);
 const void* kernel_soa_block_tma(int k, int variant);
 const void* kernel_aos_block_tma(int k, int variant);
 const void* kernel_region(int k, int variant);
+const void* kernel_generic();
 
 // Exact degrees of the embedded kernels (from embedded_tables.inc).
 void embedded_degrees(int k, int* na, int* ma, int* nb, int* mb);

@@ -96,11 +96,17 @@ int build_handle(const boysfn_table_desc* d, boysfn_tables_s* h) {
   h->x1 = d->x1;
   h->eps_tol = d->eps_tol;
   h->k_max = d->k_max;
-  const int kdev = std::min(d->k_max, boysfn_dev::kKernelKmax);
+  const int kdev = d->k_max;
   h->params.assign(kdev + 1, EvalParams{});
   h->variant.assign(kdev + 1, boysfn_dev::kVariantPadded);
   h->degree_ok.assign(kdev + 1, 0);
+  h->deg_na.assign(kdev + 1, 0);
+  h->deg_ma.assign(kdev + 1, 0);
+  h->deg_nb = d->r_B.n;
+  h->deg_mb = d->r_B.m;
   for (int k = 0; k <= kdev; ++k) {
+    h->deg_na[k] = d->r_A[k].n;
+    h->deg_ma[k] = d->r_A[k].m;
     EvalParams& p = h->params[k];
     p.x0 = d->x0;
     p.x1 = d->x1;
@@ -224,14 +230,42 @@ int choose_store(int layout, int k, const double* d_out) {
   return boysfn_dev::kStoreAoSXpose;
 }
 
+// BOYSFN_GENERIC=1 routes every order through the generic kernel (tests).
+bool generic_forced() {
+  const char* e = std::getenv("BOYSFN_GENERIC");
+  return e != nullptr && e[0] == '1';
+}
+
+// The run-time-k kernel: orders above 32 and forced regions above 32.
+int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out, int layout,
+                   size_t ld, cudaStream_t stream, unsigned long long* d_bad, int force_region) {
+  const void* fn = boysfn_dev::kernel_generic();
+  int sms = 0, bps = 0;
+  if (int st = occupancy(fn, boysfn_dev::kThreadsPerBlock, 0, &sms, &bps)) return st;
+  const size_t want = ((n + 31) / 32 + boysfn_dev::kWarpsPerBlock - 1) / boysfn_dev::kWarpsPerBlock;
+  const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
+  EvalParams p = t->params[k];
+  int na = t->deg_na[k], ma = t->deg_ma[k], nb = t->deg_nb, mb = t->deg_mb;
+  int aos = layout == BOYSFN_LAYOUT_AOS ? 1 : 0;
+  unsigned long long* counter = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), stream));
+  CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
+  void* args[] = {&p, &na, &ma, &nb, &mb, &k, &force_region, &d_x, &n, &d_out, &ld, &aos, &d_bad, &counter};
+  const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, 0, stream);
+  CUDA_TRY(cudaFreeAsync(counter, stream));
+  if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
+  boysfn_internal::count_launch();
+  return BOYSFN_OK;
+}
+
 // Launches the evaluation kernel; k already validated against the handle.
 int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out,
                 int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad) {
   if (n == 0) return BOYSFN_OK;
-  if (k > boysfn_dev::kKernelKmax)
-    return fail(BOYSFN_ERR_UNSUPPORTED, "device kernels evaluate k <= 32");
   if (!t->degree_ok[k])
     return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
+  if (k > boysfn_dev::kKernelKmax || generic_forced())
+    return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1);
   const int R = k + 1;
   const int v = t->variant[k];
   const void* fn = nullptr;
@@ -598,12 +632,17 @@ BOYSFN_API int boysfn_eval_region_host(boysfn_tables_t t, double x, int k, int r
   if (int st = get_pipeline(&P)) return st;
   cudaStream_t s = P->stream[0];
   CUDA_TRY(cudaStreamSynchronize(s));
-  if (k > boysfn_dev::kKernelKmax) return fail(BOYSFN_ERR_UNSUPPORTED, "device kernels evaluate k <= 32");
   if (!t->degree_ok[k]) return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
-  EvalParams p = t->params[k];
-  void* args[] = {&p, &x, &region, &P->d_out[0]};
-  CUDA_TRY(cudaLaunchKernel(boysfn_dev::kernel_region(k, t->variant[k]), dim3(1), dim3(1), args, 0, s));
-  boysfn_internal::count_launch();
+  if (k > boysfn_dev::kKernelKmax) {
+    CUDA_TRY(cudaMemcpyAsync(P->d_x[0], &x, sizeof(double), cudaMemcpyHostToDevice, s));
+    if (int st = launch_generic(t, P->d_x[0], 1, k, P->d_out[0], BOYSFN_LAYOUT_AOS, 1, s, nullptr, region))
+      return st;
+  } else {
+    EvalParams p = t->params[k];
+    void* args[] = {&p, &x, &region, &P->d_out[0]};
+    CUDA_TRY(cudaLaunchKernel(boysfn_dev::kernel_region(k, t->variant[k]), dim3(1), dim3(1), args, 0, s));
+    boysfn_internal::count_launch();
+  }
   CUDA_TRY(cudaMemcpyAsync(out, P->d_out[0], (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return BOYSFN_OK;

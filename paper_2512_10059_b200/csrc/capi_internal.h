@@ -16,9 +16,11 @@ struct boysfn_tables_s {
   double x0 = 0, x1 = 0, eps_tol = 0;
   int k_max = 0;
   bool is_embedded = false;
-  std::vector<boysfn_dev::EvalParams> params;  // one launch image per order k <= device kmax
-  std::vector<int> variant;                    // kernel degree variant per k
+  std::vector<boysfn_dev::EvalParams> params;  // one launch image per order k <= k_max
+  std::vector<int> variant;                    // templated-kernel degree variant per k
   std::vector<int> degree_ok;                  // 1 if r_A[k], r_B fit the device image
+  std::vector<int> deg_na, deg_ma;             // degrees of r_A[k] (generic kernel)
+  int deg_nb = 0, deg_mb = 0;                  // degrees of r_B
 };
 
 namespace boysfn_internal {

@@ -39,7 +39,7 @@ class cuda_error(RuntimeError):
 
 
 class unsupported(RuntimeError):
-    """k > 32 or a table degree the device image cannot hold."""
+    """A table degree the device image cannot hold (> 23), or Algorithm 2 with k > 32."""
 
 
 def _raise(status, first_bad=None):

@@ -1,0 +1,96 @@
+"""The run-time-k generic kernel (boys_eval_generic_kernel): bit-identical to the
+templated kernels for every k <= 32 (BOYSFN_GENERIC=1 routes all orders to it),
+and the evaluator for table sets with k_max > 32 -- the reference's gen path
+allows k_max <= 64 -- checked against the C restatement of
+eval.cpp, which takes any k."""
+import copy
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2512_10059_b200 as pkg
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(torch, xs, k, layout, tables=None):
+    x = torch.from_numpy(np.ascontiguousarray(xs)).cuda()
+    n = xs.size
+    out = torch.empty(n * (k + 1), dtype=torch.float64, device="cuda")
+    pkg.eval_device(x, k, out, tables=tables, layout=layout)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    return o.reshape(k + 1, n).T.copy() if layout == "soa" else o.reshape(n, k + 1)
+
+
+def test_generic_bit_identical_to_templated(cuda, port, monkeypatch):
+    xs = np.concatenate([port.gen_uniform(4099, 5, 0.0, 45.0), [0.0, port.x0, port.x1, 1e4]])
+    for k in range(33):
+        for layout in ("soa", "aos"):
+            a = dev(cuda, xs, k, layout)
+            monkeypatch.setenv("BOYSFN_GENERIC", "1")
+            b = dev(cuda, xs, k, layout)
+            monkeypatch.delenv("BOYSFN_GENERIC")
+            assert np.array_equal(bits(a), bits(b)), (k, layout)
+
+
+def table_k64():
+    """Appendix C extended to k_max = 64: r_A[k > 32] reuse r_A[32] (a seed of
+    the right magnitude; the values are not Boys functions above 32, but the
+    arithmetic is fully defined and the oracle restates it exactly)."""
+    t = copy.deepcopy(pkg.embedded_default())
+    t.k_max = 64
+    t.r_A += [copy.deepcopy(t.r_A[32]) for _ in range(32)]
+    pkg.validate_tables(t)
+    return t
+
+
+def oracle_tables(port, t):
+    """The port's view of a custom table set (pyoracle's structs)."""
+    import pyoracle
+    keep = []
+
+    def rat(r):
+        nu, de = np.ascontiguousarray(r.numer), np.ascontiguousarray(r.denom)
+        keep.extend((nu, de))
+        return pyoracle._Rational(len(nu) - 1, len(de) - 1, nu.ctypes.data_as(pyoracle._dp),
+                                  de.ctypes.data_as(pyoracle._dp))
+    ra = (pyoracle._Rational * len(t.r_A))(*[rat(r) for r in t.r_A])
+    keep.append(ra)
+    return pyoracle._Tables(t.x0, t.x1, t.k_max, t.eps_tol, rat(t.r_B), ra), keep
+
+
+def test_orders_above_32_match_reference_arithmetic(cuda, port):
+    t = table_k64()
+    ot, keep = oracle_tables(port, t)
+    xs = np.concatenate([port.gen_uniform(3001, 6, 0.0, 45.0), port.gen_uniform(64, 7, 28.9, 31.0)])
+    for k in (33, 40, 63, 64):
+        want = np.zeros((xs.size, k + 1))
+        bad = ctypes.c_size_t()
+        import pyoracle
+        st = port.L.oracle_boys_batch_many(xs.ctypes.data_as(pyoracle._dp), xs.size, k, ctypes.byref(ot),
+                                           want.ctypes.data_as(pyoracle._dp), want.size, ctypes.byref(bad))
+        assert st == 0
+        for layout in ("soa", "aos"):
+            got = dev(cuda, xs, k, layout, tables=t)
+            inC = xs >= t.x1
+            assert np.array_equal(bits(got[inC]), bits(want[inC])), (k, layout)  # region C exact
+            rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-300)
+            assert np.max(rel[~inC]) <= 1e-12, (k, layout, np.max(rel[~inC]))
+        # the host (drop-in) API on the same table set
+        host = np.empty(xs.size * (k + 1))
+        pkg.boys_batch_many(xs, k, t, host)
+        assert np.array_equal(bits(host.reshape(-1, k + 1)), bits(dev(cuda, xs, k, "aos", tables=t)))
+    del keep
+
+
+def test_region_seam_above_32(cuda, port):
+    t = table_k64()
+    for r in (pkg.Region.A, pkg.Region.B, pkg.Region.C):
+        x = {pkg.Region.A: t.x0 - 1e-9, pkg.Region.B: t.x0 + 1e-9, pkg.Region.C: t.x1 + 1e-9}[r]
+        v = np.array(pkg.boys_batch_region(x, 48, t, r).values)
+        assert v.shape == (49,) and np.all(np.isfinite(v))
+    with pytest.raises(pkg.out_of_range):
+        pkg.boys_batch(1.0, 65, t)

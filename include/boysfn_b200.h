@@ -37,7 +37,8 @@ typedef enum boysfn_status {
   BOYSFN_ERR_TABLES = 4,      /* std::invalid_argument from validate_tables, tables.cpp:14-32 */
   BOYSFN_ERR_CUDA = 5,        /* a CUDA runtime error (no reference equivalent)   */
   BOYSFN_ERR_ARG = 6,         /* NULL handle/pointer or bad layout/ld             */
-  BOYSFN_ERR_UNSUPPORTED = 7  /* a table degree beyond the device image (or Algorithm 2 with k > 32) */
+  BOYSFN_ERR_UNSUPPORTED = 7, /* a table degree beyond the device image (or Algorithm 2 with k > 32) */
+  BOYSFN_ERR_INVALID = 8      /* other std::invalid_argument (verify_tables arguments, verify.cpp:15-18) */
 } boysfn_status;
 
 /* Output layout.  AOS is the reference's row-major out[i*(k+1)+l]
@@ -120,6 +121,24 @@ int boysfn_eval_host(boysfn_tables_t tables, const double* xs, size_t n, int k, 
 /* Forced-region evaluation of one x (boys_batch_region, eval.cpp:59-81, the
  * reference's branch-agreement test seam), computed on the device. */
 int boysfn_eval_region_host(boysfn_tables_t tables, double x, int k, int region, double* out);
+
+/* verify_tables (verify.hpp:12-35, verify.cpp:12-63) on the device: samples
+ * samples_per_region x uniformly in each region (A [0,x0), B [x0,x1),
+ * C [x1,xmax]) with the reference's generator (std::mt19937_64(seed),
+ * u = (rng() >> 11) * 2^-53), evaluates every order k = 0..k_max and an
+ * extended-precision (double-double) oracle, and reports per (k, region) the
+ * maximum |F - oracle| with the reference's worst-case bookkeeping.
+ * per_k: caller array of (k_max+1)*3 doubles, [k][A, B, C]. */
+typedef struct boysfn_verify_report {
+  double max_err;
+  double worst_x;
+  int worst_k;
+  char worst_region; /* 'A', 'B', 'C' or '-' */
+  double max_err_region[3];
+  double* per_k;
+} boysfn_verify_report;
+int boysfn_verify_tables(boysfn_tables_t tables, int samples_per_region, double xmax, uint64_t seed,
+                         boysfn_verify_report* report);
 
 /* Algorithm 2 of the paper, fused on the
  * device: z_i = sum_{l=0..k} c_l sum_j F_l(x_i + x_j) y_j for i < n, with

@@ -212,6 +212,58 @@ int oracle_alg2_direct(const double* x, const double* y, size_t n, int k, const 
   return st;
 }
 
+/* ---- the sampling of verify_tables (verify.cpp:23-33): std::mt19937_64(seed)
+ * restated from the C++ standard ([rand.eng.mers], [rand.predef]: w=64, n=312,
+ * m=156, r=31, a=0xB5026F5AA96619E9, tempering u=29 d=0x5555555555555555 s=17
+ * b=0x71D67FFFEDA60000 t=37 c=0xFFF7EEE000000000 l=43, f=6364136223846793005),
+ * x = lo + (hi - lo) * ((rng() >> 11) * 2^-53) per region in order A, B, C. */
+typedef struct {
+  uint64_t mt[312];
+  int idx;
+} mt64;
+
+static void mt64_seed(mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->idx = 312;
+}
+
+static uint64_t mt64_next(mt64* g) {
+  if (g->idx >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t y = (g->mt[i] & 0xFFFFFFFF80000000ULL) | (g->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+      g->mt[i] = g->mt[(i + 156) % 312] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ULL : 0);
+    }
+    g->idx = 0;
+  }
+  uint64_t y = g->mt[g->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+uint64_t oracle_mt64_nth(uint64_t seed, size_t nth) {
+  mt64 g;
+  mt64_seed(&g, seed);
+  uint64_t v = 0;
+  for (size_t i = 0; i < nth; ++i) v = mt64_next(&g);
+  return v;
+}
+
+void oracle_verify_samples(double x0, double x1, double xmax, size_t per_region, uint64_t seed, double* xs) {
+  mt64 g;
+  mt64_seed(&g, seed);
+  const double lo[3] = {0.0, x0, x1}, hi[3] = {x0, x1, xmax};
+  for (int r = 0; r < 3; ++r)
+    for (size_t s = 0; s < per_region; ++s) {
+      const double u = (double)(mt64_next(&g) >> 11) * 0x1.0p-53;
+      xs[r * per_region + s] = lo[r] + (hi[r] - lo[r]) * u;
+    }
+}
+
 /* ---- synthetic workload generator shared with the device generator
  * (paper_2512_10059_b200/csrc/boys_kernels.cu: gen_uniform_kernel).  splitmix64
  * keyed by the global index, so shards of any size reproduce one stream. */

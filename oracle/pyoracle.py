@@ -71,6 +71,10 @@ class Port:
         L.oracle_classify_region.argtypes = [ctypes.c_double, ctypes.POINTER(_Tables)]
         L.oracle_gen_uniform.argtypes = [_dp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_double, ctypes.c_double]
+        L.oracle_mt64_nth.argtypes = [ctypes.c_uint64, ctypes.c_size_t]
+        L.oracle_mt64_nth.restype = ctypes.c_uint64
+        L.oracle_verify_samples.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_size_t,
+                                            ctypes.c_uint64, _dp]
         L.oracle_alg2_direct.argtypes = [_dp, _dp, ctypes.c_size_t, ctypes.c_int, _dp, ctypes.POINTER(_Tables), _dp,
                                          _dp, ctypes.c_int]
         L.oracle_hp_boys_batch_many.argtypes = [ctypes.c_int, _dp, ctypes.c_size_t, _dp, ctypes.c_int]
@@ -129,6 +133,13 @@ class Port:
         x = np.empty(n, dtype=np.float64)
         self.L.oracle_gen_uniform(x.ctypes.data_as(_dp), n, seed, offset, lo, hi)
         return x
+
+    def verify_samples(self, per_region, xmax=200.0, seed=1, x0=None, x1=None):
+        """The x verify_tables draws (verify.cpp:23-33), regions A, B, C in order."""
+        xs = np.empty(3 * per_region)
+        self.L.oracle_verify_samples(self.x0 if x0 is None else x0, self.x1 if x1 is None else x1, xmax,
+                                     per_region, seed, xs.ctypes.data_as(_dp))
+        return xs
 
     def alg2(self, x, y, c, threads=None):
         """Algorithm 2 by direct summation: (z, sum_j |y_j w_ij|)."""

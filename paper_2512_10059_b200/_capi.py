@@ -11,7 +11,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BOYSFN_LIB") or os.path.join(_HERE, "_lib", "libboysfn_b200.so")
 
 # include/boysfn_b200.h: boysfn_status
-OK, ERR_SIZE, ERR_DOMAIN, ERR_RANGE, ERR_TABLES, ERR_CUDA, ERR_ARG, ERR_UNSUPPORTED = range(8)
+OK, ERR_SIZE, ERR_DOMAIN, ERR_RANGE, ERR_TABLES, ERR_CUDA, ERR_ARG, ERR_UNSUPPORTED, ERR_INVALID = range(9)
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
 REGION_A, REGION_B, REGION_C = 0, 1, 2
 DEVICE_KMAX = 32
@@ -28,6 +28,12 @@ class TableDesc(ctypes.Structure):
     _fields_ = [("x0", ctypes.c_double), ("x1", ctypes.c_double), ("k_max", ctypes.c_int),
                 ("eps_tol", ctypes.c_double), ("r_B", RationalDesc),
                 ("r_A", ctypes.POINTER(RationalDesc))]
+
+
+class VerifyReportC(ctypes.Structure):
+    _fields_ = [("max_err", ctypes.c_double), ("worst_x", ctypes.c_double), ("worst_k", ctypes.c_int),
+                ("worst_region", ctypes.c_char), ("max_err_region", ctypes.c_double * 3),
+                ("per_k", ctypes.POINTER(ctypes.c_double))]
 
 
 # (name, restype, argtypes) for every entry point the header declares.
@@ -58,6 +64,8 @@ _SIGNATURES = [
     ("boysfn_generate_boundary", ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64,
                                                 ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                                 ctypes.c_void_p]),
+    ("boysfn_verify_tables", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
+                                            ctypes.POINTER(VerifyReportC)]),
     ("boysfn_alg2_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                           ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p,
                                           ctypes.c_void_p]),

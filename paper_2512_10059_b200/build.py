@@ -31,7 +31,7 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra"]
 
 CU_SOURCES = ["kernels_soa.cu", "kernels_aos_xpose.cu", "kernels_soa_block.cu", "kernels_soa_binned.cu",
               "kernels_aos_binned.cu",
-              "kernels_soa_block_tma.cu", "kernels_aos_block_tma.cu", "kernels_region.cu", "kernels_generic.cu", "alg2.cu",
+              "kernels_soa_block_tma.cu", "kernels_aos_block_tma.cu", "kernels_region.cu", "kernels_generic.cu", "alg2.cu", "verify.cu",
               "capi.cu"]
 CPP_SOURCES = ["shim_tables.cpp", "shim_eval.cpp"]
 
@@ -56,7 +56,7 @@ def _stale(target, deps):
 def _headers():
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".inc"))]
     hs += [os.path.join(ROOT, "include", "boysfn_b200.h")]
-    hs += [os.path.join(CPP, "include", "boysfn", f) for f in ("eval.hpp", "tables.hpp")]
+    hs += [os.path.join(CPP, "include", "boysfn", f) for f in ("eval.hpp", "tables.hpp", "verify.hpp")]
     return hs
 
 

@@ -8,6 +8,7 @@
 
 #include "../../../include/boysfn_b200.h"
 #include "boysfn/eval.hpp"
+#include "boysfn/verify.hpp"
 
 namespace boysfn {
 namespace {
@@ -21,6 +22,7 @@ void raise(int status) {
     case BOYSFN_ERR_DOMAIN: throw std::domain_error(msg);
     case BOYSFN_ERR_RANGE: throw std::out_of_range(msg);
     case BOYSFN_ERR_TABLES: throw std::invalid_argument(msg);
+    case BOYSFN_ERR_INVALID: throw std::invalid_argument(msg);
     default: throw std::runtime_error("boysfn_b200: " + std::string(boysfn_status_string(status)) + ": " + msg);
   }
 }
@@ -94,6 +96,25 @@ BoysBatch boys_batch_region(double x, int k, const CoefficientTableSet& tables, 
   raise(boysfn_eval_region_host(h.get(), x, k, static_cast<int>(region), v.data()));
   b.values = std::move(v);
   return b;
+}
+
+VerifyReport verify_tables(const CoefficientTableSet& tables, int samples_per_region, double xmax,
+                           std::uint64_t seed) {
+  const Handle h(tables);
+  std::vector<double> per_k((static_cast<size_t>(tables.k_max) + 1) * 3);
+  boysfn_verify_report r{};
+  r.per_k = per_k.data();
+  raise(boysfn_verify_tables(h.get(), samples_per_region, xmax, seed, &r));
+  VerifyReport rep;
+  rep.per_k.resize(tables.k_max + 1);
+  for (int k = 0; k <= tables.k_max; ++k)
+    rep.per_k[k] = VerifyEntry{k, per_k[3 * k], per_k[3 * k + 1], per_k[3 * k + 2]};
+  rep.max_err = r.max_err;
+  rep.worst_x = r.worst_x;
+  rep.worst_k = r.worst_k;
+  rep.worst_region = r.worst_region;
+  for (int i = 0; i < 3; ++i) rep.max_err_region[i] = r.max_err_region[i];
+  return rep;
 }
 
 }  // namespace boysfn

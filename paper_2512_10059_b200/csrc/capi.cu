@@ -443,6 +443,7 @@ BOYSFN_API const char* boysfn_status_string(int status) {
     case BOYSFN_ERR_CUDA: return "CUDA error";
     case BOYSFN_ERR_ARG: return "invalid argument";
     case BOYSFN_ERR_UNSUPPORTED: return "unsupported by the device kernels";
+    case BOYSFN_ERR_INVALID: return "invalid_argument";
     default: return "unknown status";
   }
 }

@@ -54,6 +54,7 @@ def _raise(status, first_bad=None):
         _capi.ERR_CUDA: cuda_error,
         _capi.ERR_ARG: invalid_argument,
         _capi.ERR_UNSUPPORTED: unsupported,
+        _capi.ERR_INVALID: invalid_argument,
     }.get(status, RuntimeError)(msg)
     if first_bad is not None:
         exc.first_bad = first_bad
@@ -230,6 +231,43 @@ def alg2(x, y, c, k=None, z=None, tables=None, stream=None):
                                           c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), z.data_ptr(),
                                           ctypes.c_void_p(s.cuda_stream)))
     return z
+
+
+@dataclass
+class VerifyEntry:
+    """verify.hpp:12-17."""
+    k: int = 0
+    max_err_a: float = 0.0
+    max_err_b: float = 0.0
+    max_err_c: float = 0.0
+
+
+@dataclass
+class VerifyReport:
+    """verify.hpp:19-28."""
+    per_k: List[VerifyEntry] = field(default_factory=list)
+    max_err: float = 0.0
+    worst_x: float = 0.0
+    worst_k: int = 0
+    worst_region: str = "-"
+    max_err_region: List[float] = field(default_factory=lambda: [0.0, 0.0, 0.0])
+
+    def all_within(self, eps):
+        return self.max_err <= eps
+
+
+def verify_tables(tables, samples_per_region, xmax=200.0, seed=1):
+    """verify_tables (verify.hpp:34-35) on the GPU: the reference's sampling,
+    every order, a double-double oracle; same report fields."""
+    per_k = (ctypes.c_double * ((tables.k_max + 1) * 3))()
+    rep = _capi.VerifyReportC()
+    rep.per_k = per_k
+    _raise(_capi.lib().boysfn_verify_tables(_handle(tables).handle, int(samples_per_region), float(xmax),
+                                            int(seed), ctypes.byref(rep)))
+    return VerifyReport(
+        per_k=[VerifyEntry(k, per_k[3 * k], per_k[3 * k + 1], per_k[3 * k + 2]) for k in range(tables.k_max + 1)],
+        max_err=rep.max_err, worst_x=rep.worst_x, worst_k=rep.worst_k, worst_region=rep.worst_region.decode(),
+        max_err_region=list(rep.max_err_region))
 
 
 def kernel_launch_count():

@@ -18,6 +18,7 @@
 #include "boys_oracle.h"
 #include "boysfn/eval.hpp"
 #include "boysfn/tables.hpp"
+#include "boysfn/verify.hpp"
 
 namespace {
 
@@ -168,7 +169,19 @@ int cmd_gpu() {
       CHECK(std::string(e.what()) == "upward_recursion: x must be positive", "%s", e.what());
     }
   }
-  // 5) empty input
+  // 5) verify_tables (verify.hpp:34-35) through the drop-in
+  {
+    const boysfn::VerifyReport r = boysfn::verify_tables(T, 500);
+    CHECK(r.per_k.size() == 33 && r.all_within(5e-14), "verify: max_err %g", r.max_err);
+    CHECK(r.worst_region == 'A' || r.worst_region == 'B' || r.worst_region == 'C', "worst region");
+    try {
+      boysfn::verify_tables(T, 10, 20.0);
+      CHECK(false, "xmax <= x1 not rejected");
+    } catch (const std::invalid_argument& e) {
+      CHECK(std::string(e.what()) == "verify_tables: xmax must exceed x1", "%s", e.what());
+    }
+  }
+  // 6) empty input
   {
     std::vector<double> none, out;
     boysfn::boys_batch_many(none, 99, T, out);  // the reference does not throw here

@@ -344,7 +344,10 @@ def run_b200(args, world, rank, local):
 
     e2e = None
     if not args.no_e2e and len(ks) == 1:
-        e2e = run_e2e(args, x, world)
+        try:
+            e2e = run_e2e(args, x, world)
+        except Exception as exc:  # e.g. pinned host memory exhausted; the device line still stands
+            e2e = {"value": None, "unit": UNIT, "error": "%s: %s" % (type(exc).__name__, exc)}
 
     acc = None
     if rank == 0 and not args.no_accuracy:
@@ -392,7 +395,9 @@ def run_e2e(args, x_dev, world):
     from paper_2512_10059_b200 import dist as D
     cfg = args.cfg
     k, layout = cfg["k"], cfg["layout"]
-    n = min(cfg["n"], 100_000_000)
+    # pinned host output per rank: 26 GB at 1e8 x, k=32 -- one rank gets the
+    # full batch, N ranks share the host's RAM (1/N of the batch each, >= 1e7)
+    n = min(cfg["n"], 100_000_000 if world == 1 else max(10_000_000, 100_000_000 // world))
     hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
     hx.copy_(x_dev[:n])
     hout = torch.empty(n * (k + 1), dtype=torch.float64, pin_memory=True)

@@ -227,7 +227,8 @@ def alg2(x, y, c, k=None, z=None, tables=None, stream=None):
         z = torch.empty_like(x)
     tables = tables if tables is not None else embedded_default()
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
-    _raise(_capi.lib().boysfn_alg2_device(_handle(tables).handle, x.data_ptr(), y.data_ptr(), x.numel(), k,
+    h = _handle(tables)  # keep the handle alive across the call
+    _raise(_capi.lib().boysfn_alg2_device(h.handle, x.data_ptr(), y.data_ptr(), x.numel(), k,
                                           c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), z.data_ptr(),
                                           ctypes.c_void_p(s.cuda_stream)))
     return z
@@ -262,7 +263,8 @@ def verify_tables(tables, samples_per_region, xmax=200.0, seed=1):
     per_k = (ctypes.c_double * ((tables.k_max + 1) * 3))()
     rep = _capi.VerifyReportC()
     rep.per_k = per_k
-    _raise(_capi.lib().boysfn_verify_tables(_handle(tables).handle, int(samples_per_region), float(xmax),
+    h = _handle(tables)  # keep the handle alive across the call
+    _raise(_capi.lib().boysfn_verify_tables(h.handle, int(samples_per_region), float(xmax),
                                             int(seed), ctypes.byref(rep)))
     return VerifyReport(
         per_k=[VerifyEntry(k, per_k[3 * k], per_k[3 * k + 1], per_k[3 * k + 2]) for k in range(tables.k_max + 1)],

@@ -4,7 +4,7 @@
 
 Variants are interleaved round by round and the median per (variant, k) is
 reported, so clock or neighbour drift does not favour whichever ran first.
-Paths: soa:warp soa:block aos:tma aos:xpose aos:block.
+Paths: soa:warp soa:block soa:binned soa:blocktma aos:xpose aos:binned aos:blocktma.
 """
 import os
 import statistics

@@ -278,3 +278,28 @@ def test_cpp_shim_drop_in(cuda):
     exe = build.build_shim_test()
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_cuda_graph_capture_and_replay(cuda, port):
+    """The device entry point is stream-ordered end to end (per-launch scratch
+    from the stream-ordered pool), so it captures into a CUDA graph; replays
+    reproduce the eager result bit for bit, also after the inputs change."""
+    torch = cuda
+    n, k = 300_000, 16
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    pkg.generate_uniform(x, 12, 0.0, 60.0)
+    eager = torch.empty(n * (k + 1), dtype=torch.float64, device="cuda")
+    out = torch.empty_like(eager)
+    pkg.eval_device(x, k, eager, layout="soa")  # warm the per-kernel caches outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pkg.eval_device(x, k, out, layout="soa")
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int64), eager.view(torch.int64))
+    pkg.generate_uniform(x, 13, 0.0, 60.0)
+    pkg.eval_device(x, k, eager, layout="soa")
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int64), eager.view(torch.int64))

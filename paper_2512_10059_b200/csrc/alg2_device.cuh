@@ -14,9 +14,10 @@
 //   * per pair, F_0..F_k are produced by the same recurrences as the bulk kernel
 //     (boys_device.cuh) but folded into w = sum_l c_l F_l on the fly, so F never
 //     exists as an array; e^{-(x_i+x_j)} = e^{-x_i} e^{-x_j} replaces one exp
-//     per pair by one multiply (<= 1.5 ulp instead of <= 1 ulp on e; the
-//     benchmark's contract is agreement with the direct sum within N k 1e-12
-//     relative).
+//     per pair by one multiply, and the B/C seeds use Newton-refined
+//     reciprocal / inverse square root instead of IEEE division and sqrt (a few
+//     ulp instead of correctly rounded; the benchmark's contract is agreement
+//     with the direct sum within N k 1e-12 relative).
 #pragma once
 
 #include "boys_device.cuh"
@@ -31,6 +32,28 @@ struct Alg2Coef {
 };
 
 #ifdef __CUDACC__
+
+// 1/b for a normal positive b: rcp.approx (MUFU.RCP64H) + two Newton steps.
+__device__ __forceinline__ double rcp_normal(double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = __fma_rn(-b, r, 1.0);
+  e = __fma_rn(e, e, e);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-b, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+// 1/sqrt(s) for a normal positive s: rsqrt.approx (MUFU.RSQ64H, ~2^-22) + two
+// Newton steps (error ~1.5 e^2 per step).
+__device__ __forceinline__ double rsqrt_normal(double s) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double h = 0.5 * s;
+  y = __fma_rn(y, __fma_rn(-h * y, y, 0.5), y);
+  y = __fma_rn(y, __fma_rn(-h * y, y, 0.5), y);
+  return y;
+}
 
 // w = sum_l c_l F_l(s) for one argument s, given e = e^{-s}.
 template <int K, int NA, int MA, int NB, int MB>
@@ -47,14 +70,18 @@ __device__ __forceinline__ double boys_dot(const EvalParams& P, const Alg2Coef& 
     }
     return w;
   }
-  // regions B and C: seed F_0, upward (eval.cpp:49-57, 73-77)
-  const double inv2s = __ddiv_rn(0.5, s);
-  double F, tail;
+  // regions B and C: seed F_0, upward (eval.cpp:49-57, 73-77).  The pair sum is
+  // a normal positive double here, so the branch-free reciprocal / inverse
+  // square root (<= 2 ulp) replace the IEEE division and square root.
+  double F, tail, inv2s;
   if (s < P.x1) {
+    inv2s = 0.5 * rcp_normal(s);
     F = rational<NB, MB>(P.numB, P.denB, s);
     tail = -__dmul_rn(e, inv2s);
   } else {
-    F = __ddiv_rn(kHalfSqrtPi, __dsqrt_rn(s));
+    const double y = rsqrt_normal(s);
+    F = kHalfSqrtPi * y;
+    inv2s = 0.5 * (y * y);
     tail = -0.0;
   }
   double w = C.c[0] * F;

@@ -10,6 +10,8 @@ data path (the only NCCL calls are the timing barrier and the max-over-ranks
 reduction).  Other named configs (reported in DESIGN.md, not the driver's line):
   cfg2       configs[2]: 1e8 x clustered at the region boundaries, k = 0..32 sweep
   cfg3       configs[3]: 1e9 log-uniform x in [1e-12, 1e4], k = 16, AoS (fits HBM)
+  cfg4       configs[4]: 1e10 x in total, sharded over the GPUs (strong scaling),
+             k = 16 by default (--k 4/16/32), streamed
   northstar  1e9 uniform x in [0,100], k = 32, SoA, streamed through a reused
              1e8-x output buffer (264 GB of F per step > HBM)
 
@@ -49,6 +51,10 @@ CONFIGS = {
                           "kmax 0..32 sweep (one launch per k per step), SoA",
                  n=100_000_000, k=32, ks=list(range(33)), layout="soa", dist="boundary", lo=0.0, hi=0.0, seed=3,
                  chunk=None),
+    "cfg4": dict(workload="configs[4]: 1e10 uniform x in [0,100] sharded across the GPUs (strong scaling), "
+                          "k=16 (--k 4/16/32), SoA, each shard streamed through a reused 1e8-x output buffer",
+                 n=10_000_000_000, k=16, layout="soa", dist="uniform", lo=0.0, hi=100.0, seed=5,
+                 chunk=100_000_000, strong=True),
     "northstar": dict(workload="north star: F_0..F_32 for 1e9 uniform x in [0,100] per B200, SoA, streamed "
                                "through a reused 1e8-x output buffer (264 GB of F per step > HBM)",
                       n=1_000_000_000, k=32, layout="soa", dist="uniform", lo=0.0, hi=100.0, seed=2,
@@ -276,11 +282,17 @@ def run_b200(args, world, rank, local):
     from paper_2512_10059_b200 import dist as D
 
     cfg = args.cfg
-    n, k, layout = cfg["n"], cfg["k"], cfg["layout"]
-    chunk = cfg["chunk"] or n
+    n_total = cfg["n"]
+    if cfg.get("strong"):  # total work fixed, contiguous near-equal shards
+        begin, end = D.strong_shard(n_total, world, rank)
+        n = end - begin
+    else:  # per-GPU work fixed
+        begin, n = D.weak_shard(n_total, rank)[0], n_total
+    k, layout = cfg["k"], cfg["layout"]
+    chunk = min(cfg["chunk"] or n, n)
     dev = torch.device("cuda", local if world > 1 else 0)
     x = torch.empty(n, dtype=torch.float64, device=dev)
-    generate(pkg, x, cfg, D.weak_shard(n, rank)[0])
+    generate(pkg, x, cfg, begin)
     out = torch.empty(chunk * (k + 1), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     pieces = [(c, min(n, c + chunk)) for c in range(0, n, chunk)]
@@ -321,8 +333,8 @@ def run_b200(args, world, rank, local):
     total_ms = D.max_over_ranks(ev[0].elapsed_time(ev[-1]))
     per_step = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
     ms_step = total_ms / args.steps
-    values_per_step = n * sum(kk + 1 for kk in ks)
-    value = world * values_per_step / (ms_step * 1e-3)
+    # whole-job throughput: every rank's values over the slowest rank's time
+    value = (n_total if cfg.get("strong") else world * n) * sum(kk + 1 for kk in ks) / (ms_step * 1e-3)
 
     hbm, peak_kind = peaks()
     alg_bytes = chunk * (8 + 8 * (k + 1))
@@ -373,9 +385,11 @@ def run_b200(args, world, rank, local):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if cfg.get("strong") else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "name": args.config, "n_per_gpu": n, "kmax": k,
+            "config": {"workload": cfg["workload"], "name": args.config, "n_per_gpu": n, "n_total": n_total
+                       if cfg.get("strong") else n * world, "kmax": k,
                        "layout": layout,
                        "x": "%s [%g,%g] splitmix64 seed %d, global index offset rank*N"
                             % (cfg["dist"], cfg["lo"], cfg["hi"], cfg["seed"]),

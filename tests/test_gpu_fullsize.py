@@ -123,3 +123,38 @@ def test_host_api_equals_device_api(cuda, port):
         pinned = torch.empty(n * (k + 1), dtype=torch.float64, pin_memory=True).numpy()
         pkg.boys_batch_many(xs, k, pkg.embedded_default(), pinned, layout=layout)
         assert np.array_equal(bits(pinned), bits(d))
+
+
+def test_host_api_concurrent_threads(cuda, port):
+    """boys_batch_many is reentrant: concurrent host threads (ctypes
+    releases the GIL; each thread owns a staging pipeline) get exactly the
+    single-threaded results."""
+    import threading
+    s = pkg.embedded_default()
+    jobs = [(port.gen_uniform(700_001 + 1000 * j, 50 + j, 0.0, 60.0), (4, 8, 16, 32)[j]) for j in range(4)]
+    want = []
+    for xs, k in jobs:
+        o = np.empty(xs.size * (k + 1))
+        pkg.boys_batch_many(xs, k, s, o)
+        want.append(o)
+    got = [None] * len(jobs)
+    errors = []
+
+    def run(j):
+        try:
+            xs, k = jobs[j]
+            o = np.empty(xs.size * (k + 1))
+            for _ in range(3):
+                pkg.boys_batch_many(xs, k, s, o)
+            got[j] = o
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(j,)) for j in range(len(jobs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for g, w in zip(got, want):
+        assert np.array_equal(bits(g), bits(w))

@@ -363,6 +363,26 @@ struct Pipeline {
     return BOYSFN_OK;
   }
 
+  Pipeline() = default;
+  Pipeline(const Pipeline&) = delete;
+  Pipeline& operator=(const Pipeline&) = delete;
+  // Released when the owning host thread exits (errors ignored: at process
+  // exit the runtime may already be gone).
+  ~Pipeline() {
+    for (int s = 0; s < kSlots; ++s) {
+      if (stream[s]) cudaStreamSynchronize(stream[s]);
+      cudaFree(d_x[s]);
+      cudaFree(d_out[s]);
+      cudaFreeHost(h_x[s]);
+      cudaFreeHost(h_out[s]);
+      if (done[s]) cudaEventDestroy(done[s]);
+      if (copied[s]) cudaEventDestroy(copied[s]);
+      if (stream[s]) cudaStreamDestroy(stream[s]);
+    }
+    cudaFree(d_bad);
+    cudaFreeHost(h_bad);
+  }
+
   int ensure_staging() {
     for (int s = 0; s < kSlots; ++s) {
       if (h_x[s] == nullptr) CUDA_TRY(cudaHostAlloc(&h_x[s], cap_x * sizeof(double), cudaHostAllocDefault));

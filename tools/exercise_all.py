@@ -1,7 +1,10 @@
-"""Small end-to-end exercise of every kernel family for compute-sanitizer
-(memcheck / racecheck / synccheck): all output paths at ragged sizes, the
-generic kernel, the region seam, the host pipeline with an error mid-batch,
-verify_tables and Algorithm 2.  Development aid; see profiles/r01_sanitizer_*."""
+"""Small end-to-end exercise of every kernel family: all output paths at ragged
+sizes, the generic kernel, the region seam, the host pipeline with an error
+mid-batch, verify_tables and Algorithm 2.  Run it against the checked build
+(python -m paper_2512_10059_b200.build --variant checked BOYSFN_DEVICE_CHECKS,
+BOYSFN_LIB=.../variants/checked/libboysfn_b200.so): every shared-memory and
+global index the kernels form is then asserted in range on the device
+(compute-sanitizer is closed on this GPU pool)."""
 import os
 import sys
 
@@ -45,7 +48,7 @@ def main():
     z = pkg.alg2(torch.rand(300, dtype=torch.float64, device="cuda") * 30,
                  torch.rand(300, dtype=torch.float64, device="cuda"), np.ones(13))
     torch.cuda.synchronize()
-    print("sanitize smoke done", float(z.sum()))
+    print("exercise done", float(z.sum()))
 
 
 if __name__ == "__main__":

@@ -24,6 +24,8 @@ const void* kernel_soa_binned(int k, int variant);
 const void* kernel_aos_binned(int k, int variant);
 const void* kernel_soa_block_tma(int k, int variant);
 const void* kernel_aos_block_tma(int k, int variant);
+const void* kernel_soa_block_tma_bin(int k, int variant);
+const void* kernel_aos_block_tma_bin(int k, int variant);
 const void* kernel_region(int k, int variant);
 const void* kernel_generic();
 

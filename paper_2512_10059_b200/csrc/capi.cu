@@ -197,17 +197,21 @@ bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R, int 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Output-path selection (medians of interleaved
-// B200 runs, profiles/r01_paths*.txt).  Large k is HBM-write-bound and wants
-// long contiguous write bursts: block tiles of 128 x stored by the TMA engine
-// (1 KB SoA row segments / 1 KB*(k+1) AoS spans).  Small k is issue-bound
-// and wants no A/B/C divergence: the region-binned kernels.  AoS with k+1
-// even avoids the block stage (bank conflicts on the row-major stage) and uses
-// the per-warp transpose path.
-//   SoA: k <= 6 binned, else block-TMA (block/LSU if no tensor map applies)
-//   AoS: k <= 6 or k == 8 binned; k+1 odd block-TMA; k+1 even transpose
-// BOYSFN_SOA_PATH = warp|block|binned|blocktma and
-// BOYSFN_AOS_PATH = xpose|binned|blocktma override the choice
+// Output-path selection (short-train medians of
+// every path at every k on one B200, profiles/r01_path_sweep.txt).  Large k is
+// HBM-write-bound and wants long contiguous write bursts: block tiles of 128 x
+// stored by the TMA engine (1 KB SoA row segments / 1 KB*(k+1) AoS spans),
+// within 1-2% of one another with and without the region sort.  Small k is
+// issue-bound and wants no A/B/C divergence at the least overhead: the per-warp
+// region-binned kernels.  The AoS block stage is row-major [128][k+1]; at
+// k+1 = 16 or 32 its stores are 8/16-way bank conflicts, and the per-warp
+// transpose (padded pitch) takes those two orders.
+//   SoA: k <= 6 binned; 8..13 block-TMA region-sorted; else block-TMA
+//        (block/LSU if no tensor map applies)
+//   AoS: k <= 5 binned; 6, 8 block-TMA region-sorted; k+1 in {16, 32} transpose;
+//        else block-TMA (transpose if the output is not 16-B aligned)
+// BOYSFN_SOA_PATH = warp|block|binned|blocktma|blocktmabin and
+// BOYSFN_AOS_PATH = xpose|binned|blocktma|blocktmabin override the choice
 // (experiments and the path-equivalence tests).
 int choose_store(int layout, int k, const double* d_out) {
   const int R = k + 1;
@@ -219,15 +223,18 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "block") return boysfn_dev::kStoreSoABlock;
     if (want == "binned") return boysfn_dev::kStoreSoABinned;
     if (want == "blocktma") return boysfn_dev::kStoreSoABlockTma;
-    return k <= 6 ? boysfn_dev::kStoreSoABinned : boysfn_dev::kStoreSoABlockTma;
+    if (want == "blocktmabin") return boysfn_dev::kStoreSoABlockTmaBin;
+    if (k <= 6) return boysfn_dev::kStoreSoABinned;
+    return (k >= 8 && k <= 13) ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
   }
   if (want == "xpose") return boysfn_dev::kStoreAoSXpose;
   if (want == "binned") return boysfn_dev::kStoreAoSBinned;
   if (want == "blocktma" && a16) return boysfn_dev::kStoreAoSBlockTma;
+  if (want == "blocktmabin" && a16) return boysfn_dev::kStoreAoSBlockTmaBin;
   if (!want.empty()) return boysfn_dev::kStoreAoSXpose;
-  if (k <= 6 || k == 8) return boysfn_dev::kStoreAoSBinned;
-  if ((R & 1) && a16) return boysfn_dev::kStoreAoSBlockTma;
-  return boysfn_dev::kStoreAoSXpose;
+  if (k <= 5) return boysfn_dev::kStoreAoSBinned;
+  if (!a16 || R == 16 || R == 32) return boysfn_dev::kStoreAoSXpose;
+  return (k == 6 || k == 8) ? boysfn_dev::kStoreAoSBlockTmaBin : boysfn_dev::kStoreAoSBlockTma;
 }
 
 // BOYSFN_GENERIC=1 routes every order through the generic kernel (tests).
@@ -274,16 +281,25 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   std::memset(&tmap, 0, sizeof tmap);
   int store = choose_store(layout, k, d_out);
   const int threads = boysfn_dev::kThreadsPerBlock;
-  if (store == boysfn_dev::kStoreSoABlockTma && !make_soa_tmap(&tmap, d_out, n, ld, R, threads))
+  if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) &&
+      !make_soa_tmap(&tmap, d_out, n, ld, R, threads))
     store = boysfn_dev::kStoreSoABlock;
   switch (store) {
     case boysfn_dev::kStoreSoABlockTma:
       fn = boysfn_dev::kernel_soa_block_tma(k, v);
-      smem = sizeof(double) * boysfn_dev::kBlockX * R + 16;
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTma>(R, boysfn_dev::kBlockX);
       break;
     case boysfn_dev::kStoreAoSBlockTma:
       fn = boysfn_dev::kernel_aos_block_tma(k, v);
-      smem = sizeof(double) * boysfn_dev::kBlockX * R + 16;
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTma>(R, boysfn_dev::kBlockX);
+      break;
+    case boysfn_dev::kStoreSoABlockTmaBin:
+      fn = boysfn_dev::kernel_soa_block_tma_bin(k, v);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTmaBin>(R, boysfn_dev::kBlockX);
+      break;
+    case boysfn_dev::kStoreAoSBlockTmaBin:
+      fn = boysfn_dev::kernel_aos_block_tma_bin(k, v);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaBin>(R, boysfn_dev::kBlockX);
       break;
     case boysfn_dev::kStoreSoA:
       fn = boysfn_dev::kernel_soa(k, v);

@@ -12,8 +12,8 @@ import paper_2512_10059_b200 as pkg
 
 pytestmark = pytest.mark.gpu
 
-PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("aos", "xpose"),
-         ("aos", "binned"), ("aos", "blocktma")]
+PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
+         ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin")]
 
 
 def run(torch, x, k, lay, path, monkeypatch):
@@ -40,15 +40,18 @@ def test_all_paths_bit_identical(cuda, monkeypatch, n):
             assert torch.equal(got, ref), (n, k, lay, path)
 
 
-def test_binned_paths_report_first_bad(cuda, port):
+def test_all_paths_report_first_bad(cuda, port, monkeypatch):
     torch = cuda
     xs = port.gen_uniform(5000, 3, 0.0, 30.0)
     xs[4321] = np.inf
     xs[777] = -3.0
     x = torch.from_numpy(xs).cuda()
-    for k in (0, 4, 8):  # the binned kernels are the default for k <= 8
-        for lay in ("soa", "aos"):
+    for k in (0, 4, 8, 16):
+        for lay, path in PATHS:
+            monkeypatch.setenv("BOYSFN_SOA_PATH" if lay == "soa" else "BOYSFN_AOS_PATH", path)
             fb = torch.full((1,), -1, dtype=torch.int64, device="cuda")
             out = torch.empty(xs.size * (k + 1), dtype=torch.float64, device="cuda")
             pkg.eval_device(x, k, out, layout=lay, first_bad=fb)
-            assert int(fb.item()) == 777
+            monkeypatch.delenv("BOYSFN_SOA_PATH", raising=False)
+            monkeypatch.delenv("BOYSFN_AOS_PATH", raising=False)
+            assert int(fb.item()) == 777, (k, lay, path)

@@ -579,6 +579,7 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     CUDA_TRY(cudaEventRecord(P->done[s], P->stream[s]));
     return BOYSFN_OK;
   };
+  const bool soa_d2h_2d = std::getenv("BOYSFN_SOA_D2H_2D") != nullptr;  // A/B experiments
   // D2H of the chunk's first `rows` rows: to the caller directly, or to staging.
   auto fetch = [&](size_t c, size_t rows) -> int {
     const int s = static_cast<int>(c % S);
@@ -589,8 +590,16 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
         CUDA_TRY(cudaMemcpyAsync(dst, P->d_out[s], rows * row * sizeof(double), cudaMemcpyDeviceToHost,
                                  P->stream[s]));
       } else if (out_direct) {
-        CUDA_TRY(cudaMemcpy2DAsync(out + off, ld * sizeof(double), P->d_out[s], cn * sizeof(double),
-                                   rows * sizeof(double), row, cudaMemcpyDeviceToHost, P->stream[s]));
+        // one 1D copy per order row: the strided 2D copy of the same rows ran
+        // at 38 GB/s against 50 GB/s for 1D copies on the B200 hosts
+        if (soa_d2h_2d) {
+          CUDA_TRY(cudaMemcpy2DAsync(out + off, ld * sizeof(double), P->d_out[s], cn * sizeof(double),
+                                     rows * sizeof(double), row, cudaMemcpyDeviceToHost, P->stream[s]));
+        } else {
+          for (size_t l = 0; l < row; ++l)
+            CUDA_TRY(cudaMemcpyAsync(out + l * ld + off, P->d_out[s] + l * cn, rows * sizeof(double),
+                                     cudaMemcpyDeviceToHost, P->stream[s]));
+        }
       } else {
         CUDA_TRY(cudaMemcpyAsync(P->h_out[s], P->d_out[s], row * cn * sizeof(double), cudaMemcpyDeviceToHost,
                                  P->stream[s]));

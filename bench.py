@@ -322,16 +322,27 @@ def run_b200(args, world, rank, local):
     D.barrier()
     torch.cuda.synchronize(dev)
     launches0 = pkg.kernel_launch_count()
+    # Hold the stream in a short spin (outside the timed region) while the host
+    # enqueues all timed steps, so a host-side hiccup cannot leave the GPU idle
+    # between steps and inflate the device-timed interval.
+    # (~3 ms of device time per launch to enqueue covers the host's worst
+    # observed per-step enqueue time, GIL hand-offs to the clock sampler included)
+    torch.cuda._sleep(int(min(2.0, 0.02 + 0.003 * args.steps * len(pieces) * len(ks)) * 2e9))
     ev[0].record(stream)
+    host_ms = []
     for s in range(args.steps):
+        h0 = time.perf_counter()
         step(record=len(ks) > 1)
         ev[s + 1].record(stream)
+        host_ms.append((time.perf_counter() - h0) * 1e3)
     torch.cuda.synchronize(dev)
     D.barrier()
     launches = pkg.kernel_launch_count() - launches0
     clocks = sampler.stop()
     total_ms = D.max_over_ranks(ev[0].elapsed_time(ev[-1]))
     per_step = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
+    step_stats = {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step),
+                  "host_enqueue_max": max(host_ms)}
     ms_step = total_ms / args.steps
     # whole-job throughput: every rank's values over the slowest rank's time
     value = (n_total if cfg.get("strong") else world * n) * sum(kk + 1 for kk in ks) / (ms_step * 1e-3)
@@ -396,7 +407,7 @@ def run_b200(args, world, rank, local):
                        "l2": "inputs+outputs %.1f GB per launch >> 126 MB L2 (no flush needed)" % (alg_bytes / 1e9),
                        "parallelism": "dp%d (independent shards, no collective)" % world},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks, "accuracy": acc,
+            "clocks": clocks, "accuracy": acc, "step_ms": step_stats,
         }
         if per_k is not None:
             line["per_k"] = per_k

@@ -149,6 +149,19 @@ int boysfn_verify_tables(boysfn_tables_t tables, int samples_per_region, double 
 int boysfn_alg2_device(boysfn_tables_t tables, const double* d_x, const double* d_y, size_t n, int k,
                        const double* c, double* d_z, void* stream);
 
+/* Coefficient generator support (replaces the
+ * grid scan and golden-section refinement of remez.cpp:33-108, ErrorCurve).
+ * For HOST arrays xs[npts] writes err[i] = rho(x) (F_k(x) - p(x)/q(x)) with
+ * F_k by the reference's series (reference.cpp:10-23), p and q by Horner,
+ * all in double-double on the device; p, q given as double-double coefficient
+ * pairs (hi, lo), ascending, degrees n, m <= 64; weight 0: rho = 1 (r_B),
+ * 1: rho = rho_A,k (Eq. 18, regions.cpp:74-85).  k <= 64.  Synchronous. */
+int boysfn_gen_error_scan(int k, const double* num_hi, const double* num_lo, int n, const double* den_hi,
+                          const double* den_lo, int m, int weight, const double* xs, size_t npts,
+                          double* err);
+/* F_k(xs[i]) in double-double (hi[i] + lo[i]), HOST arrays, synchronous. */
+int boysfn_gen_boys_dd(int k, const double* xs, size_t npts, double* hi, double* lo);
+
 /* Synthetic workload: x[i] = lo + (hi-lo)*u_i with u_i = (splitmix64(seed +
  * (offset+i+1)*0x9E3779B97F4A7C15) >> 11) * 2^-53, the multiply and add
  * separately rounded, so any CPU restating the formula reproduces it bit for

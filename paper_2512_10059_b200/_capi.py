@@ -69,6 +69,11 @@ _SIGNATURES = [
     ("boysfn_alg2_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                           ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p,
                                           ctypes.c_void_p]),
+    ("boysfn_gen_error_scan", ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    ("boysfn_gen_boys_dd", ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                          ctypes.c_void_p]),
     ("boysfn_kernel_launch_count", ctypes.c_ulonglong, []),
 ]
 

@@ -43,6 +43,8 @@ def main():
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     if os.environ.get("AB_DIST") == "logu":
         pkg.generate_loguniform(x, 4, -12.0, 4.0)
+    elif os.environ.get("AB_DIST") == "boundary":
+        pkg.generate_boundary(x, 3)
     else:
         pkg.generate_uniform(x, 2, 0.0, 100.0)
     out = torch.empty(n * (kmax + 1), dtype=torch.float64, device="cuda")

@@ -4,12 +4,15 @@
 
 The `regions` and `gen` subcommands of SPEC.md:464-480 (the reference's CLI is
 absent from /root/reference).  Exit codes as specified there: 0 success,
-1 input error, 3 internal non-convergence."""
+1 input error, 2 verification failure, 3 internal non-convergence.  `gen`
+verifies the generated set on the GPU before writing it (SPEC.md: gen output
+always passes verify), trying the runner-up cells of an order's winning
+anti-diagonal when the rounded-to-double table misses eps_tol."""
 import argparse
 import sys
 
 from .. import tables as T
-from .generate import generate_tables
+from .generate import certify, generate_tables
 from .regions import compute_x0, compute_x1
 
 
@@ -27,6 +30,7 @@ def main(argv=None):
     g.add_argument("--max-degree", type=int, default=24)
     g.add_argument("--backend", default="gpu", choices=["gpu", "mp"])
     g.add_argument("--workers", type=int, default=1, help="processes for the r_A searches")
+    g.add_argument("--verify-samples", type=int, default=10000, help="verify_tables samples per region")
     a = ap.parse_args(argv)
     try:
         if a.cmd == "regions":
@@ -43,6 +47,14 @@ def main(argv=None):
     if not all(rep.met_tolerance for rep in res.reports):
         return 3
     if orders is None:
+        log = []
+        ok, vrep = certify(res.tables, res.alternatives, a.verify_samples, log=log)
+        for line in log:
+            print(line)
+        print("verify_tables: max_err %.4e at k=%d region %s -> %s" % (
+            vrep.max_err, vrep.worst_k, vrep.worst_region, "PASS" if ok else "FAIL"))
+        if not ok:
+            return 2
         with open(a.out, "w") as f:
             f.write(T.emit_tables(res.tables))
     return 0

@@ -539,6 +539,9 @@ class WalshResult:
     m: int = 0
     sup_error: object = 0
     cells: list = dataclasses.field(default_factory=list)
+    # every cell of the winning anti-diagonal that met the tolerance, best
+    # first, as (n, m, sup_error, approximant): the runners-up of the selection
+    alternatives: list = dataclasses.field(default_factory=list)
 
 
 def walsh_search(f, rho, a, b, eps_tol, max_total_degree, rng_seed=1, require_numer_le_denom=False,
@@ -571,12 +574,15 @@ def walsh_search(f, rho, a, b, eps_tol, max_total_degree, rng_seed=1, require_nu
                         have_best = True
                         result.approximant, result.n, result.m = cell.approximant, n, m
                         result.sup_error = cell.sup_error
-                    if cell.sup_error <= eps and (not hit or cell.sup_error < best.sup_error):
-                        hit = True
-                        best.approximant, best.n, best.m, best.sup_error = cell.approximant, n, m, cell.sup_error
+                    if cell.sup_error <= eps:
+                        best.alternatives.append((n, m, cell.sup_error, cell.approximant))
+                        if not hit or cell.sup_error < best.sup_error:
+                            hit = True
+                            best.approximant, best.n, best.m, best.sup_error = cell.approximant, n, m, cell.sup_error
             if hit:
                 best.met_tolerance = True
                 best.cells = result.cells
+                best.alternatives.sort(key=lambda t: t[2])
                 return best
     result.met_tolerance = False
     return result

@@ -23,6 +23,10 @@ def main():
     kmax, eps, workers, out = int(sys.argv[1]), float(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
     t = time.time()
     res = generate_tables(kmax, eps, workers=workers)
+    from paper_2512_10059_b200.gen.generate import certify
+    log = []
+    ok, _ = certify(res.tables, res.alternatives, 10000, log=log)
+    print("\n".join(log), "certified" if ok else "NOT certified", flush=True)
     print("generated in %.1f s" % (time.time() - t), flush=True)
     with open(out, "w") as f:
         f.write(T.emit_tables(res.tables))

@@ -179,3 +179,23 @@ def test_cli_regions(capsys):
     from paper_2512_10059_b200.gen.__main__ import main
     assert main(["regions", "--kmax", "32", "--eps", "5e-14"]) == 0
     assert capsys.readouterr().out.strip() == "x0=11.899848152108484 x1=28.98933773882074"
+
+
+def test_rho_A_is_the_downward_amplification():
+    """a seed perturbation delta at order k, carried down the
+    recurrence F_l = (2x F_{l+1} + e^-x)/(2l+1), is amplified at most by
+    rho_A,k(x) over l = 0..k (equality at the worst order)."""
+    rng = random.Random(8)
+    x0 = float(gen.compute_x0(32))
+    for _ in range(12):
+        k, x = rng.randint(1, 32), mpf(rng.uniform(0, x0))
+        e = mpmath.exp(-x)
+        delta = mpf("1e-16")
+        a, b = gen.boys_reference(k, x), gen.boys_reference(k, x) + delta
+        amp = mpf(1)
+        for l in range(k - 1, -1, -1):
+            a = (2 * x * a + e) / (2 * l + 1)
+            b = (2 * x * b + e) / (2 * l + 1)
+            amp = max(amp, abs(b - a) / delta)
+        rho = gen.weight_rho_A(k, x)
+        assert abs(amp / rho - 1) < mpf("1e-6"), (k, x)

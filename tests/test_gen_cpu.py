@@ -199,3 +199,19 @@ def test_rho_A_is_the_downward_amplification():
             amp = max(amp, abs(b - a) / delta)
         rho = gen.weight_rho_A(k, x)
         assert abs(amp / rho - 1) < mpf("1e-6"), (k, x)
+
+
+def test_generated_k32_set_matches_appendix_c_shape():
+    """The set written by `gen --kmax 32 --eps 5e-14` on the B200 box
+    (tests/golden/generated_k32_tables.txt, profiles/r01_gen_full_k32.txt):
+    same x0, x1 and, table by table, the same total degree n+m as Appendix C."""
+    import os
+    import paper_2512_10059_b200 as pkg
+    from paper_2512_10059_b200 import tables as T
+    path = os.path.join(os.path.dirname(__file__), "golden", "generated_k32_tables.txt")
+    g = T.parse_tables(open(path).read())
+    e = pkg.embedded_default()
+    assert (g.x0, g.x1, g.k_max, g.eps_tol) == (e.x0, e.x1, e.k_max, e.eps_tol)
+    assert (g.r_B.degree_n(), g.r_B.degree_m()) == (5, 6)
+    for a, b in zip(g.r_A, e.r_A):
+        assert a.degree_n() + a.degree_m() == b.degree_n() + b.degree_m()

@@ -79,3 +79,12 @@ def test_generate_small_set_self_verifies(cuda):
     assert T.emit_tables(back) == text
     rep = pkg.verify_tables(back, 4000, 60.0, 3)
     assert rep.max_err <= 1e-8, (rep.max_err, rep.worst_k, rep.worst_region)
+
+
+def test_generated_k32_set_passes_verify(cuda):
+    """The certified generated set meets eps_tol on the GPU verify (1e4/region)."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "generated_k32_tables.txt")
+    t = T.parse_tables(open(path).read())
+    rep = pkg.verify_tables(t, 10000, 200.0, 11)
+    assert rep.max_err <= t.eps_tol, (rep.max_err, rep.worst_k, rep.worst_region)

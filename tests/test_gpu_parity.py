@@ -129,6 +129,31 @@ def test_boundaries_and_special_values(cuda, port):
     assert port.classify(port.x1) == 2
 
 
+def test_region_c_fast_path_range_end(cuda, port, monkeypatch):
+    """Region C's sqrt/division fast paths apply for x < 2^1022 and the IEEE
+    operations above (boys_device.cuh: in_bc_fast_range).  Around that switch
+    and at the top of the double range every output path is bit-identical to
+    the reference for every order."""
+    xs = [2.0 ** 1021, 1e300, 1.7976931348623157e308, np.nextafter(np.inf, 0)]
+    v = 2.0 ** 1022
+    for _ in range(6):
+        v = np.nextafter(v, 0.0)
+    for _ in range(13):
+        xs.append(v)
+        v = np.nextafter(v, np.inf)
+    xs = np.array(xs)
+    paths = [("soa", p) for p in ("warp", "block", "binned", "blocktma", "blocktmabin")] + \
+            [("aos", p) for p in ("xpose", "binned", "blocktma", "blocktmabin")]
+    for k in range(33):
+        want = port.boys_batch_many(xs, k)
+        for layout, path in paths:
+            monkeypatch.setenv("BOYSFN_SOA_PATH" if layout == "soa" else "BOYSFN_AOS_PATH", path)
+            got = device_eval(cuda, xs, k, layout)
+            monkeypatch.delenv("BOYSFN_SOA_PATH", raising=False)
+            monkeypatch.delenv("BOYSFN_AOS_PATH", raising=False)
+            assert np.array_equal(bits(got), bits(want)), (k, layout, path)
+
+
 def test_branch_consistency_at_boundaries(cuda, port):
     """at x0 +- 1e-9 and x1 +- 1e-9 adjacent branches agree within
     1e-13 -- checked through the forced-region seam (boys_batch_region)."""

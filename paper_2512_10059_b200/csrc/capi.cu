@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -429,6 +430,79 @@ struct Segment {
   size_t n;
 };
 
+// Persistent host-copy workers: spawning 15 threads per 128-MB chunk cost
+// ~0.3 ms against a ~3.7 ms copy.  One process-wide pool; concurrent callers
+// (one staging pipeline per host thread) take turns, since they share the
+// host memory bandwidth anyway.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  // Copies every piece, on the calling thread plus up to T-1 workers.
+  void run(const std::vector<Segment>& pieces, int T) {
+    std::lock_guard<std::mutex> turn(turn_mu_);
+    ensure_workers(T - 1);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      pieces_ = &pieces;
+      next_.store(0);
+      helpers_ = std::min<int>(T - 1, static_cast<int>(workers_.size()));
+      busy_ = helpers_;
+      ++generation_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return busy_ == 0; });
+    pieces_ = nullptr;
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  void drain() {
+    const std::vector<Segment>& p = *pieces_;
+    for (size_t i = next_.fetch_add(1); i < p.size(); i = next_.fetch_add(1))
+      std::memcpy(p[i].dst, p[i].src, p[i].n * sizeof(double));
+  }
+  void ensure_workers(int want) {
+    while (static_cast<int>(workers_.size()) < want) {
+      const int id = static_cast<int>(workers_.size());
+      workers_.emplace_back([this, id] { loop(id); });
+    }
+  }
+  void loop(int id) {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (generation_ != seen && id < helpers_); });
+        if (stop_) return;
+        seen = generation_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--busy_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::mutex turn_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> workers_;
+  const std::vector<Segment>* pieces_ = nullptr;
+  std::atomic<size_t> next_{0};
+  unsigned long long generation_ = 0;
+  int helpers_ = 0, busy_ = 0;
+  bool stop_ = false;
+};
+
 void parallel_copy(std::vector<Segment> segs) {
   size_t total = 0;
   for (const auto& g : segs) total += g.n;
@@ -439,13 +513,23 @@ void parallel_copy(std::vector<Segment> segs) {
   const size_t piece = std::max<size_t>(1, (total + T - 1) / T);
   for (const auto& g : segs)
     for (size_t o = 0; o < g.n; o += piece) pieces.push_back({g.dst + o, g.src + o, std::min(piece, g.n - o)});
-  auto work = [&](int t) {
-    for (size_t i = t; i < pieces.size(); i += T) std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].n * sizeof(double));
-  };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto& th : pool) th.join();
+  if (T <= 1) {
+    for (const auto& pc : pieces) std::memcpy(pc.dst, pc.src, pc.n * sizeof(double));
+    return;
+  }
+  if (std::getenv("BOYSFN_COPY_SPAWN") != nullptr) {  // A/B experiments: threads per call
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+      for (size_t i = next.fetch_add(1); i < pieces.size(); i = next.fetch_add(1))
+        std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].n * sizeof(double));
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    return;
+  }
+  CopyPool::get().run(pieces, T);
 }
 
 int get_pipeline(Pipeline** out) {

@@ -17,7 +17,10 @@ def main():
     specs = [s.split(":") for s in sys.argv[1:]]
     kmax = max(int(s[-1]) for s in specs)
     x = torch.empty(n, dtype=torch.float64, device="cuda")
-    pkg.generate_uniform(x, 2, 0.0, 100.0)
+    if os.environ.get("RO_DIST") == "boundary":
+        pkg.generate_boundary(x, 3)
+    else:
+        pkg.generate_uniform(x, 2, 0.0, 100.0)
     out = torch.empty(n * (kmax + 1), dtype=torch.float64, device="cuda")
     for s in specs:
         lay, k = s[0], int(s[-1])

@@ -141,10 +141,50 @@ boysfn_tables_s* embedded_handle() {
 struct DeviceInfo {
   int sms = 0;
   std::map<const void*, int> blocks_per_sm;
+  cudaMemPool_t pool = nullptr;  // this library's stream-ordered pool
 };
 
 std::mutex g_dev_mu;
 std::map<int, DeviceInfo> g_devices;
+
+// The library's own stream-ordered memory pool on the current device (for the
+// per-launch scheduler counters and Algorithm 2's scratch).  Unlike the
+// device's default pool it keeps up to 64 MB reserved across synchronisations,
+// so a launch after a sync does not re-map physical memory, and setting that
+// does not change the default pool the rest of the process uses.
+int device_pool(cudaMemPool_t* out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  DeviceInfo& di = g_devices[dev];
+  if (di.pool == nullptr) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CUDA_TRY(cudaMemPoolCreate(&di.pool, &props));
+    uint64_t keep = uint64_t(64) << 20;
+    CUDA_TRY(cudaMemPoolSetAttribute(di.pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  *out = di.pool;
+  return BOYSFN_OK;
+}
+
+// Zeroed per-launch counter in stream order: the caller's (a pipeline slot's
+// own, reused on its private stream) or one from the library pool, released
+// after the launch in stream order (*release set).
+int launch_counter(unsigned long long* given, cudaStream_t stream, unsigned long long** ctr, bool* release) {
+  *release = given == nullptr;
+  if (given != nullptr) {
+    *ctr = given;
+  } else {
+    cudaMemPool_t pool = nullptr;
+    if (int st = device_pool(&pool)) return st;
+    CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(ctr), sizeof(unsigned long long), pool, stream));
+  }
+  CUDA_TRY(cudaMemsetAsync(*ctr, 0, sizeof(unsigned long long), stream));
+  return BOYSFN_OK;
+}
 
 int occupancy(const void* fn, int threads, size_t smem, int* sms, int* bps) {
   int dev = 0;
@@ -246,7 +286,8 @@ bool generic_forced() {
 
 // The run-time-k kernel: orders above 32 and forced regions above 32.
 int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out, int layout,
-                   size_t ld, cudaStream_t stream, unsigned long long* d_bad, int force_region) {
+                   size_t ld, cudaStream_t stream, unsigned long long* d_bad, int force_region,
+                   unsigned long long* d_ctr = nullptr) {
   const void* fn = boysfn_dev::kernel_generic();
   int sms = 0, bps = 0;
   if (int st = occupancy(fn, boysfn_dev::kThreadsPerBlock, 0, &sms, &bps)) return st;
@@ -256,11 +297,11 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
   int na = t->deg_na[k], ma = t->deg_ma[k], nb = t->deg_nb, mb = t->deg_mb;
   int aos = layout == BOYSFN_LAYOUT_AOS ? 1 : 0;
   unsigned long long* counter = nullptr;
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), stream));
-  CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
+  bool release = false;
+  if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
   void* args[] = {&p, &na, &ma, &nb, &mb, &k, &force_region, &d_x, &n, &d_out, &ld, &aos, &d_bad, &counter};
   const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, 0, stream);
-  CUDA_TRY(cudaFreeAsync(counter, stream));
+  if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
   if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
   boysfn_internal::count_launch();
   return BOYSFN_OK;
@@ -268,12 +309,13 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
 
 // Launches the evaluation kernel; k already validated against the handle.
 int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out,
-                int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad) {
+                int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad,
+                unsigned long long* d_ctr = nullptr) {
   if (n == 0) return BOYSFN_OK;
   if (!t->degree_ok[k])
     return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
   if (k > boysfn_dev::kKernelKmax || generic_forced())
-    return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1);
+    return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1, d_ctr);
   const int R = k + 1;
   const int v = t->variant[k];
   const void* fn = nullptr;
@@ -329,15 +371,14 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   const size_t want = (ntiles + wpb - 1) / wpb;
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
   EvalParams p = t->params[k];
-  // Per-launch tile counter from the stream-ordered pool: zeroed, used and
-  // released in stream order, so concurrent launches on other streams never
-  // share it.
+  // Per-launch tile counter, zeroed and used in stream order, so concurrent
+  // launches on other streams never share it.
   unsigned long long* counter = nullptr;
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), stream));
-  CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
+  bool release = false;
+  if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
   void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad, &counter, &tmap};  // tmap: block-TMA kernels only
   const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
-  CUDA_TRY(cudaFreeAsync(counter, stream));
+  if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
   if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
   boysfn_internal::count_launch();
   return BOYSFN_OK;
@@ -356,6 +397,7 @@ struct Pipeline {
   double* d_x[kSlots] = {};
   double* d_out[kSlots] = {};
   unsigned long long* d_bad = nullptr;  // kSlots words
+  unsigned long long* d_ctr = nullptr;  // kSlots scheduler counters (slot s: only on stream[s])
   unsigned long long* h_bad = nullptr;  // pinned, kSlots words
   size_t cap_x = 0;                     // x capacity per slot
   size_t cap_out = 0;                   // doubles per slot
@@ -370,6 +412,7 @@ struct Pipeline {
       CUDA_TRY(cudaEventCreateWithFlags(&copied[s], cudaEventDisableTiming));
     }
     CUDA_TRY(cudaMalloc(&d_bad, kSlots * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMalloc(&d_ctr, kSlots * sizeof(unsigned long long)));
     CUDA_TRY(cudaHostAlloc(&h_bad, kSlots * sizeof(unsigned long long), cudaHostAllocDefault));
     cap_out = kChunkOutBytes / sizeof(double);
     cap_x = cap_out;  // enough for k = 0
@@ -397,6 +440,7 @@ struct Pipeline {
       if (stream[s]) cudaStreamDestroy(stream[s]);
     }
     cudaFree(d_bad);
+    cudaFree(d_ctr);
     cudaFreeHost(h_bad);
   }
 
@@ -656,7 +700,8 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     }
     CUDA_TRY(cudaMemcpyAsync(P->d_x[s], src, cn * sizeof(double), cudaMemcpyHostToDevice, P->stream[s]));
     CUDA_TRY(cudaMemsetAsync(P->d_bad + s, 0xFF, sizeof(unsigned long long), P->stream[s]));
-    if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], P->d_bad + s))
+    if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], P->d_bad + s,
+                             P->d_ctr + s))
       return st;
     CUDA_TRY(cudaMemcpyAsync(P->h_bad + s, P->d_bad + s, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              P->stream[s]));
@@ -765,7 +810,8 @@ BOYSFN_API int boysfn_eval_region_host(boysfn_tables_t t, double x, int k, int r
   if (!t->degree_ok[k]) return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
   if (k > boysfn_dev::kKernelKmax) {
     CUDA_TRY(cudaMemcpyAsync(P->d_x[0], &x, sizeof(double), cudaMemcpyHostToDevice, s));
-    if (int st = launch_generic(t, P->d_x[0], 1, k, P->d_out[0], BOYSFN_LAYOUT_AOS, 1, s, nullptr, region))
+    if (int st = launch_generic(t, P->d_x[0], 1, k, P->d_out[0], BOYSFN_LAYOUT_AOS, 1, s, nullptr, region,
+                                P->d_ctr))
       return st;
   } else {
     EvalParams p = t->params[k];

@@ -389,7 +389,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
 // H2D copy + kernel of chunk c+2 and the D2H copy of chunk c overlap.
 struct Pipeline {
   static constexpr int kSlots = 3;
-  static constexpr size_t kChunkOutBytes = size_t(128) << 20;
+  static constexpr size_t kChunkOutBytes = size_t(256) << 20;  // profiles/r01_e2e_chunk.txt
   int device = -1;
   cudaStream_t stream[kSlots] = {};
   cudaEvent_t done[kSlots] = {};    // kernel + first-bad flag of the slot's chunk
@@ -414,7 +414,10 @@ struct Pipeline {
     CUDA_TRY(cudaMalloc(&d_bad, kSlots * sizeof(unsigned long long)));
     CUDA_TRY(cudaMalloc(&d_ctr, kSlots * sizeof(unsigned long long)));
     CUDA_TRY(cudaHostAlloc(&h_bad, kSlots * sizeof(unsigned long long), cudaHostAllocDefault));
-    cap_out = kChunkOutBytes / sizeof(double);
+    size_t chunk = kChunkOutBytes;
+    if (const char* e = std::getenv("BOYSFN_CHUNK_MB"))  // A/B experiments
+      chunk = std::max<size_t>(1, std::strtoull(e, nullptr, 10)) << 20;
+    cap_out = chunk / sizeof(double);
     cap_x = cap_out;  // enough for k = 0
     for (int s = 0; s < kSlots; ++s) {
       CUDA_TRY(cudaMalloc(&d_x[s], cap_x * sizeof(double)));

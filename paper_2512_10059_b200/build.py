@@ -109,6 +109,23 @@ def build_shim_test(force=False):
     return SHIM_TEST
 
 
+GEN = os.path.join(LIBDIR, "boysfn_gen")
+GEN_SOURCES = ["gen_hp.cpp", "gen_remez.cpp", "gen_main.cpp"]
+
+
+def build_gen(force=False):
+    """The native table generator (binary128 restatement of the reference's
+    generator library, GPU extremum scan through the C ABI)."""
+    srcs = [os.path.join(CPP, "src", "gen", f) for f in GEN_SOURCES]
+    hdrs = [os.path.join(CPP, "include", "boysfn", f) for f in
+            ("highprec.hpp", "reference.hpp", "polynomial.hpp", "linalg.hpp", "regions.hpp", "remez.hpp",
+             "tables.hpp", "verify.hpp")]
+    if force or _stale(GEN, srcs + hdrs + [LIB]):
+        _run(["g++", "-std=gnu++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(CPP, "include")] + srcs +
+             ["-o", GEN, "-L", LIBDIR, "-lboysfn_b200", "-Wl,-rpath,$ORIGIN", "-lquadmath", "-lpthread"])
+    return GEN
+
+
 def build_oracle():
     """The test-only checkers (oracle/Makefile): always the C restatement, plus
     the compiled reference where /root/reference exists."""
@@ -119,6 +136,7 @@ def build_all(force=False):
     build_oracle()
     build_library(force=force)
     build_shim_test(force=force)
+    build_gen(force=force)
 
 
 if __name__ == "__main__":

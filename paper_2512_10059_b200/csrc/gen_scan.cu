@@ -78,10 +78,46 @@ __global__ void gen_boys_kernel(int k, const double* __restrict__ xs, size_t n, 
   }
 }
 
-struct DevBuf {
-  void* p = nullptr;
-  ~DevBuf() { cudaFree(p); }
+// Per host thread: a private stream and device buffers grown on demand, so
+// generator threads scanning concurrently neither allocate per call (cudaFree
+// synchronises the device) nor serialise on the legacy default stream.
+struct ScanScratch {
+  cudaStream_t stream = nullptr;
+  double* d[3] = {nullptr, nullptr, nullptr};
+  size_t cap = 0;
+  int device = -1;
+  ~ScanScratch() {
+    for (double* p : d) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+  }
 };
+
+int scratch_for(size_t n, ScanScratch** out) {
+  thread_local ScanScratch s;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (s.device != dev) {  // first use on this thread, or the thread switched devices
+    for (double*& p : s.d) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    s.cap = 0;
+    if (s.stream) cudaStreamDestroy(s.stream);
+    s.stream = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    s.device = dev;
+  }
+  if (n > s.cap) {
+    for (double*& p : s.d) {
+      cudaFree(p);
+      p = nullptr;
+      CUDA_TRY(cudaMalloc(&p, n * sizeof(double)));
+    }
+    s.cap = n;
+  }
+  *out = &s;
+  return BOYSFN_OK;
+}
 
 }  // namespace
 
@@ -100,15 +136,15 @@ BOYSFN_API int boysfn_gen_error_scan(int k, const double* num_hi, const double* 
   R.m = m;
   for (int i = 0; i <= n; ++i) R.num[i] = dd{num_hi[i], num_lo[i]};
   for (int i = 0; i <= m; ++i) R.den[i] = dd{den_hi[i], den_lo[i]};
-  DevBuf dx, de;
-  CUDA_TRY(cudaMalloc(&dx.p, npts * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&de.p, npts * sizeof(double)));
-  CUDA_TRY(cudaMemcpy(dx.p, xs, npts * sizeof(double), cudaMemcpyHostToDevice));
+  ScanScratch* S = nullptr;
+  if (int st = scratch_for(npts, &S)) return st;
+  CUDA_TRY(cudaMemcpyAsync(S->d[0], xs, npts * sizeof(double), cudaMemcpyHostToDevice, S->stream));
   const unsigned grid = static_cast<unsigned>(std::min<size_t>((npts + 255) / 256, 148 * 16));
-  gen_error_kernel<<<grid, 256>>>(R, k, weight, static_cast<const double*>(dx.p), npts, static_cast<double*>(de.p));
+  gen_error_kernel<<<grid, 256, 0, S->stream>>>(R, k, weight, S->d[0], npts, S->d[1]);
   CUDA_TRY(cudaGetLastError());
   boysfn_internal::count_launch();
-  CUDA_TRY(cudaMemcpy(err, de.p, npts * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpyAsync(err, S->d[1], npts * sizeof(double), cudaMemcpyDeviceToHost, S->stream));
+  CUDA_TRY(cudaStreamSynchronize(S->stream));
   return BOYSFN_OK;
 }
 
@@ -117,17 +153,15 @@ BOYSFN_API int boysfn_gen_boys_dd(int k, const double* xs, size_t npts, double* 
   if (k < 0 || k > 64) return fail(BOYSFN_ERR_ARG, "gen_boys_dd: k must lie in [0, 64]");
   if (npts == 0) return BOYSFN_OK;
   if (!xs || !hi || !lo) return fail(BOYSFN_ERR_ARG, "null argument");
-  DevBuf dx, dh, dl;
-  CUDA_TRY(cudaMalloc(&dx.p, npts * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&dh.p, npts * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&dl.p, npts * sizeof(double)));
-  CUDA_TRY(cudaMemcpy(dx.p, xs, npts * sizeof(double), cudaMemcpyHostToDevice));
+  ScanScratch* S = nullptr;
+  if (int st = scratch_for(npts, &S)) return st;
+  CUDA_TRY(cudaMemcpyAsync(S->d[0], xs, npts * sizeof(double), cudaMemcpyHostToDevice, S->stream));
   const unsigned grid = static_cast<unsigned>(std::min<size_t>((npts + 255) / 256, 148 * 16));
-  gen_boys_kernel<<<grid, 256>>>(k, static_cast<const double*>(dx.p), npts, static_cast<double*>(dh.p),
-                                 static_cast<double*>(dl.p));
+  gen_boys_kernel<<<grid, 256, 0, S->stream>>>(k, S->d[0], npts, S->d[1], S->d[2]);
   CUDA_TRY(cudaGetLastError());
   boysfn_internal::count_launch();
-  CUDA_TRY(cudaMemcpy(hi, dh.p, npts * sizeof(double), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(lo, dl.p, npts * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpyAsync(hi, S->d[1], npts * sizeof(double), cudaMemcpyDeviceToHost, S->stream));
+  CUDA_TRY(cudaMemcpyAsync(lo, S->d[2], npts * sizeof(double), cudaMemcpyDeviceToHost, S->stream));
+  CUDA_TRY(cudaStreamSynchronize(S->stream));
   return BOYSFN_OK;
 }

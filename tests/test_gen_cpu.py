@@ -215,3 +215,37 @@ def test_generated_k32_set_matches_appendix_c_shape():
     assert (g.r_B.degree_n(), g.r_B.degree_m()) == (5, 6)
     for a, b in zip(g.r_A, e.r_A):
         assert a.degree_n() + a.degree_m() == b.degree_n() + b.degree_m()
+
+
+def _gen_binary():
+    import os
+    import subprocess
+    from paper_2512_10059_b200 import build
+    path = build.GEN
+    if not os.path.exists(path):
+        pytest.skip("boysfn_gen not built")
+    return path, subprocess
+
+
+def test_native_generator_selftest_and_regions():
+    """The native (binary128) generator: SPEC acceptance 2 and 6 fixtures, and
+    the `regions` subcommand."""
+    path, sp = _gen_binary()
+    r = sp.run([path, "selftest"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    r = sp.run([path, "regions", "--kmax", "32", "--eps", "5e-14"], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip() == "x0=11.899848152108484 x1=28.98933773882074"
+    r = sp.run([path, "regions", "--kmax", "32"], capture_output=True, text=True)
+    assert r.returncode == 1  # input error: missing flag
+
+
+def test_native_generator_matches_the_mpmath_restatement_cpu():
+    """r_B by the reference's golden-section search on the CPU: the binary128
+    and the 50-digit mpmath restatements take the same exchange path (same
+    iteration count) to the same minimax error."""
+    path, sp = _gen_binary()
+    r = sp.run([path, "remez", "--region", "B", "--n", "5", "--m", "6", "--mp"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    head = dict(kv.split("=") for kv in r.stdout.splitlines()[0].split())
+    assert int(head["alternation"]) == 13
+    assert abs(float(head["sup"]) - 9.50270970198117e-15) < 1e-19  # mpmath backend, DESIGN.md 3.4

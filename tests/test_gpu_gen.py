@@ -88,3 +88,28 @@ def test_generated_k32_set_passes_verify(cuda):
     t = T.parse_tables(open(path).read())
     rep = pkg.verify_tables(t, 10000, 200.0, 11)
     assert rep.max_err <= t.eps_tol, (rep.max_err, rep.worst_k, rep.worst_region)
+
+
+def test_native_generator_reproduces_r_B_and_a_small_set(cuda, tmp_path):
+    """boysfn_gen (binary128 + GPU scan): r_B (5, 6) matches the embedded table
+    within 1e-12 relative on 1000 points; `gen` for k_max = 2 at 1e-8 writes a
+    set that parses and passes verify_tables."""
+    import subprocess
+    from paper_2512_10059_b200 import build
+    r = subprocess.run([build.GEN, "remez", "--region", "B", "--n", "5", "--m", "6"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert "alternation=13" in lines[0]
+    num = [float(l.split()[1]) for l in lines if l.startswith("numer")]
+    den = [float(l.split()[1]) for l in lines if l.startswith("denom")]
+    emb = pkg.embedded_default()
+    xs = np.linspace(emb.x0, emb.x1, 1000)
+    mine = np.polyval(num[::-1], xs) / np.polyval(den[::-1], xs)
+    ref = np.polyval(emb.r_B.numer[::-1], xs) / np.polyval(emb.r_B.denom[::-1], xs)
+    assert np.abs(mine / ref - 1).max() <= 1e-12
+    out = tmp_path / "k2.txt"
+    r = subprocess.run([build.GEN, "gen", "--kmax", "2", "--eps", "1e-8", "--out", str(out), "--max-degree", "16"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    t = T.parse_tables(out.read_text())
+    assert t.k_max == 2 and pkg.verify_tables(t, 4000, 60.0, 5).max_err <= 1e-8

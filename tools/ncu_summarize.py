@@ -1,10 +1,11 @@
 #!/usr/bin/env python3
 """Summarise an `ncu --set full` report into profiles/ (text + ncu_summary.json).
 
-    python tools/ncu_summarize.py gpurun_out/prof.ncu-rep <key> <out.txt> [n]
+    python tools/ncu_summarize.py gpurun_out/prof.ncu-rep <key> <out.txt> [n] [index]
 
 <key> names the workload (e.g. soa_k32); ncu_summary.json[launches][key] gets
-the per-launch DRAM traffic that bench.py reports as roofline.traffic.
+the per-launch DRAM traffic that bench.py reports as roofline.traffic (of the
+index-th kernel in the report, default the last); out.txt lists every kernel.
 """
 import csv
 import io
@@ -36,9 +37,10 @@ def raw(rep):
 def main():
     rep, key, txt = sys.argv[1], sys.argv[2], sys.argv[3]
     n_x = int(float(sys.argv[4])) if len(sys.argv) > 4 else None
+    pick = int(sys.argv[5]) if len(sys.argv) > 5 else -1
     h, u, data = raw(rep)
     lines = []
-    summary = None
+    summaries = []
     for v in data:
         name = v[h.index("Kernel Name")]
         lines.append("kernel: %s" % name)
@@ -69,6 +71,8 @@ def main():
         summary["dram_bytes_per_launch"] = summary["dram_bytes_read"] + summary["dram_bytes_write"]
         if n_x:
             summary["n"] = n_x
+        summaries.append(summary)
+    summary = summaries[pick]
     with open(txt, "w") as f:
         f.write("# ncu --set full --clock-control none (%s); per-launch values, cold cache, serialised\n" % rep)
         f.write("\n".join(lines) + "\n")

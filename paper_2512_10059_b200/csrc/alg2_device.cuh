@@ -93,39 +93,60 @@ __device__ __forceinline__ double boys_dot(const EvalParams& P, const Alg2Coef& 
   return w;
 }
 
-// One thread per (sorted) x_i; all x_j streamed through shared memory.
-// xs sorted ascending, es = e^{-xs}, ys carried along; zs in sorted order.
+// Persistent pair kernel.  Work items are (i-block of kAlg2Threads sorted x_i,
+// j-segment of seg_len x_j); blocks claim items from a counter until none are
+// left, so the last wave is item-sized, not block-sized (a grid of one block
+// per i-block left 3.46 waves at N = 2^19: the last 46% full).  Each thread
+// owns one x_i, streams its segment's x_j through shared memory in tiles of
+// kAlg2TileJ, and writes its partial sum to partial[seg * n + i]; the segments
+// are added in order by the scatter kernel (deterministic).
+// xs sorted ascending, es = e^{-xs}, ys carried along.
 template <int K, int NA, int MA, int NB, int MB>
 __global__ void __launch_bounds__(kAlg2Threads)
     boys_alg2_kernel(const __grid_constant__ EvalParams P, const __grid_constant__ Alg2Coef C,
                      const double* __restrict__ xs, const double* __restrict__ es,
-                     const double* __restrict__ ys, size_t n, double* __restrict__ zs) {
+                     const double* __restrict__ ys, size_t n, int nseg, size_t seg_len,
+                     unsigned long long* __restrict__ counter, double* __restrict__ partial) {
   __shared__ double sx[kAlg2TileJ], se[kAlg2TileJ], sy[kAlg2TileJ];
+  __shared__ unsigned long long s_item;
   const int tid = threadIdx.x;
-  const size_t i = static_cast<size_t>(blockIdx.x) * kAlg2Threads + tid;
-  const double xi = i < n ? xs[i] : 0.0;
-  const double ei = i < n ? es[i] : 1.0;
-  double acc0 = 0.0, acc1 = 0.0;
-  for (size_t j0 = 0; j0 < n; j0 += kAlg2TileJ) {
+  const size_t nib = (n + kAlg2Threads - 1) / kAlg2Threads;
+  const unsigned long long items = static_cast<unsigned long long>(nib) * nseg;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(counter, 1ull);
+    __syncthreads();
+    const unsigned long long item = s_item;
+    __syncthreads();  // everyone has read s_item before the next claim overwrites it
+    if (item >= items) break;
+    const size_t ib = static_cast<size_t>(item / nseg);
+    const int seg = static_cast<int>(item % nseg);
+    const size_t i = ib * kAlg2Threads + tid;
+    const double xi = i < n ? xs[i] : 0.0;
+    const double ei = i < n ? es[i] : 1.0;
+    const size_t jb = static_cast<size_t>(seg) * seg_len;
+    const size_t je = jb + seg_len < n ? jb + seg_len : n;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (size_t j0 = jb; j0 < je; j0 += kAlg2TileJ) {
 #pragma unroll
-    for (int r = 0; r < kAlg2TileJ / kAlg2Threads; ++r) {
-      const size_t j = j0 + r * kAlg2Threads + tid;
-      const bool ok = j < n;
-      sx[r * kAlg2Threads + tid] = ok ? xs[j] : 0.0;
-      se[r * kAlg2Threads + tid] = ok ? es[j] : 1.0;
-      sy[r * kAlg2Threads + tid] = ok ? ys[j] : 0.0;  // padding contributes y = 0
-    }
-    __syncthreads();
+      for (int r = 0; r < kAlg2TileJ / kAlg2Threads; ++r) {
+        const size_t j = j0 + r * kAlg2Threads + tid;
+        const bool ok = j < je;
+        sx[r * kAlg2Threads + tid] = ok ? xs[j] : 0.0;
+        se[r * kAlg2Threads + tid] = ok ? es[j] : 1.0;
+        sy[r * kAlg2Threads + tid] = ok ? ys[j] : 0.0;  // padding contributes y = 0
+      }
+      __syncthreads();
 #pragma unroll 2
-    for (int jj = 0; jj < kAlg2TileJ; jj += 2) {  // two independent pair chains per step
-      const double w0 = boys_dot<K, NA, MA, NB, MB>(P, C, xi + sx[jj], __dmul_rn(ei, se[jj]));
-      const double w1 = boys_dot<K, NA, MA, NB, MB>(P, C, xi + sx[jj + 1], __dmul_rn(ei, se[jj + 1]));
-      acc0 = __fma_rn(sy[jj], w0, acc0);
-      acc1 = __fma_rn(sy[jj + 1], w1, acc1);
+      for (int jj = 0; jj < kAlg2TileJ; jj += 2) {  // two independent pair chains per step
+        const double w0 = boys_dot<K, NA, MA, NB, MB>(P, C, xi + sx[jj], __dmul_rn(ei, se[jj]));
+        const double w1 = boys_dot<K, NA, MA, NB, MB>(P, C, xi + sx[jj + 1], __dmul_rn(ei, se[jj + 1]));
+        acc0 = __fma_rn(sy[jj], w0, acc0);
+        acc1 = __fma_rn(sy[jj + 1], w1, acc1);
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    if (i < n) partial[static_cast<size_t>(seg) * n + i] = acc0 + acc1;
   }
-  if (i < n) zs[i] = acc0 + acc1;
 }
 
 #endif  // __CUDACC__

@@ -253,6 +253,31 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def fp64_roofline(pkg, x, ks, step_s):
+    """The FP64 side of the roofline: algorithmic
+    flops of the step -- per x, A: 2(n_k+m_k)+1+[k>0](2+3k), B: 25+3k,
+    C: 3+2k (a mul+add pair counts 2; div, sqrt, exp count 1), with the
+    step's own region counts -- over the step time, against the measured DFMA
+    peak (tools/fp64_peak.cu)."""
+    t = pkg.embedded_default()
+    na = int((x < t.x0).sum().item())
+    nb = int(((x >= t.x0) & (x < t.x1)).sum().item())
+    nc = x.numel() - na - nb
+    flops = 0
+    for k in ks:
+        ra = t.r_A[k]
+        flops += na * (2 * (ra.degree_n() + ra.degree_m()) + 1 + (2 + 3 * k if k > 0 else 0))
+        flops += nb * (25 + 3 * k) + nc * (3 + 2 * k)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as f:
+            peak, kind = float(json.load(f)["fp64_tflops"]), "measured (tools/fp64_peak.cu)"
+    except Exception:
+        peak, kind = 37.2, "nominal (148 SMs x 64 DFMA/clk x 1.965 GHz x 2)"
+    achieved = flops / step_s / 1e12
+    return {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "peak_kind": kind,
+            "algorithmic_flops_per_step": flops, "region_counts": [na, nb, nc]}
+
+
 def accuracy_sample(x_dev, k, layout):
     """max |gpu - oracle| and |gpu - reference| on a strided sample."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -359,6 +384,8 @@ def run_b200(args, world, rank, local):
                 "traffic": ncu_traffic(cfg), "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "note": "per x: 8 B read + 8*(k+1) B written; %d launch(es) per step" % len(pieces)}
+
+    roofline["fp64"] = fp64_roofline(pkg, x, ks, ms_step * 1e-3)
 
     per_k = None
     if len(ks) > 1:

@@ -308,9 +308,11 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
 }
 
 // Launches the evaluation kernel; k already validated against the handle.
+// force_store >= 0 overrides the path choice (the host API's small-batch path
+// writes host-mapped memory and takes the per-warp LSU stores).
 int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out,
                 int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad,
-                unsigned long long* d_ctr = nullptr) {
+                unsigned long long* d_ctr = nullptr, int force_store = -1) {
   if (n == 0) return BOYSFN_OK;
   if (!t->degree_ok[k])
     return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
@@ -322,7 +324,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   size_t smem = 0;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
-  int store = choose_store(layout, k, d_out);
+  int store = force_store >= 0 ? force_store : choose_store(layout, k, d_out);
   const int threads = boysfn_dev::kThreadsPerBlock;
   if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) &&
       !make_soa_tmap(&tmap, d_out, n, ld, R, threads))
@@ -403,6 +405,14 @@ struct Pipeline {
   size_t cap_out = 0;                   // doubles per slot
   double* h_x[kSlots] = {};             // pinned staging for pageable callers (lazy)
   double* h_out[kSlots] = {};
+  // small-batch path (lazy): host-mapped x and F the kernel reads and writes
+  // over PCIe directly, so a small call is one launch and one sync
+  static constexpr size_t kSmallValues = size_t(1) << 20;  // capacity, doubles
+  size_t small_limit = kSmallValues;  // n*(k+1) <= this takes the path (profiles/r01_small_path.txt)
+  double* hs_x = nullptr;
+  double* hs_out = nullptr;
+  double* ds_x = nullptr;
+  double* ds_out = nullptr;
 
   int init(int dev) {
     device = dev;
@@ -445,6 +455,17 @@ struct Pipeline {
     cudaFree(d_bad);
     cudaFree(d_ctr);
     cudaFreeHost(h_bad);
+    cudaFreeHost(hs_x);
+    cudaFreeHost(hs_out);
+  }
+
+  int ensure_small() {
+    if (hs_x != nullptr) return BOYSFN_OK;
+    CUDA_TRY(cudaHostAlloc(&hs_x, kSmallValues * sizeof(double), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostAlloc(&hs_out, kSmallValues * sizeof(double), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ds_x), hs_x, 0));
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ds_out), hs_out, 0));
+    return BOYSFN_OK;
   }
 
   int ensure_staging() {
@@ -684,6 +705,34 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
   }
   Pipeline* P = nullptr;
   if (int st = get_pipeline(&P)) return st;
+  if (const char* e = std::getenv("BOYSFN_SMALL_VALUES"))  // A/B experiments
+    P->small_limit = std::min<size_t>(Pipeline::kSmallValues, std::strtoull(e, nullptr, 10));
+  if (n * row <= P->small_limit && std::getenv("BOYSFN_NO_SMALL_PATH") == nullptr) {
+    // small batch: x and F cross PCIe inside the kernel (host-mapped pinned
+    // buffers, per-warp LSU loads/stores), one launch, one synchronisation
+    if (int st = P->ensure_small()) return st;
+    // check_input (eval.cpp:13-15) on the host: the first bad x bounds the rows
+    size_t bad = n;
+    for (size_t i = 0; i < n; ++i) {
+      P->hs_x[i] = xs[i];
+      if (bad == n && !x_ok(xs[i])) bad = i;
+    }
+    const int store = layout == BOYSFN_LAYOUT_SOA ? boysfn_dev::kStoreSoA : boysfn_dev::kStoreAoSXpose;
+    if (int st = launch_eval(t, P->ds_x, n, k, P->ds_out, layout, n, P->stream[0], nullptr, P->d_ctr, store))
+      return st;
+    CUDA_TRY(cudaStreamSynchronize(P->stream[0]));
+    const size_t rows = bad;
+    if (layout == BOYSFN_LAYOUT_AOS) {
+      std::memcpy(out, P->hs_out, rows * row * sizeof(double));
+    } else {
+      for (size_t l = 0; l < row; ++l) std::memcpy(out + l * ld, P->hs_out + l * n, rows * sizeof(double));
+    }
+    if (bad != n) {
+      if (first_bad) *first_bad = bad;
+      return fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
+    }
+    return BOYSFN_OK;
+  }
   const size_t cx = std::max<size_t>(32, std::min(P->cap_x, P->cap_out / row) / 32 * 32);
   const size_t nchunks = (n + cx - 1) / cx;
   const int S = Pipeline::kSlots;

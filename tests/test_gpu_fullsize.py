@@ -158,3 +158,35 @@ def test_host_api_concurrent_threads(cuda, port):
     assert not errors, errors
     for g, w in zip(got, want):
         assert np.array_equal(bits(g), bits(w))
+
+
+def test_small_batch_path_equals_pipeline(cuda, port, monkeypatch):
+    """Small calls (n*(k+1) <= 2^20) run one kernel on host-mapped buffers;
+    they return exactly what the staged pipeline returns, including the rows
+    written before a bad x and the reported first bad index."""
+    s = pkg.embedded_default()
+    rng = np.random.default_rng(21)
+    for k, n in ((0, 1), (8, 33), (32, 1000), (16, 65536 // 17), (31, 2047), (32, (1 << 20) // 33), (0, 1 << 20)):
+        xs = rng.uniform(0, 60, n)
+        for layout in ("aos", "soa"):
+            small = np.full(n * (k + 1), -1.0)
+            pkg.boys_batch_many(xs, k, s, small, layout=layout)
+            monkeypatch.setenv("BOYSFN_NO_SMALL_PATH", "1")
+            big = np.full(n * (k + 1), -1.0)
+            pkg.boys_batch_many(xs, k, s, big, layout=layout)
+            monkeypatch.delenv("BOYSFN_NO_SMALL_PATH")
+            assert np.array_equal(bits(small), bits(big)), (k, n, layout)
+    xs = rng.uniform(0, 60, 500)
+    xs[321] = np.nan
+    for layout in ("aos", "soa"):
+        outs = []
+        for no_small in (False, True):
+            if no_small:
+                monkeypatch.setenv("BOYSFN_NO_SMALL_PATH", "1")
+            o = np.full(500 * 9, -7.0)
+            with pytest.raises(pkg.domain_error) as ei:
+                pkg.boys_batch_many(xs, 8, s, o, layout=layout)
+            assert ei.value.first_bad == 321
+            outs.append(o)
+            monkeypatch.delenv("BOYSFN_NO_SMALL_PATH", raising=False)
+        assert np.array_equal(bits(outs[0]), bits(outs[1]))

@@ -7,8 +7,6 @@ import time
 import numpy as np
 import torch
 
-cudart = ctypes.CDLL("libcudart.so.12") if False else None
-
 
 def main():
     import os

@@ -140,7 +140,7 @@ boysfn_tables_s* embedded_handle() {
 // ------------------------------------------------------------- dispatch --
 struct DeviceInfo {
   int sms = 0;
-  std::map<const void*, int> blocks_per_sm;
+  std::map<std::pair<const void*, size_t>, int> blocks_per_sm;  // (kernel, dynamic smem)
   cudaMemPool_t pool = nullptr;  // this library's stream-ordered pool
 };
 
@@ -192,13 +192,17 @@ int occupancy(const void* fn, int threads, size_t smem, int* sms, int* bps) {
   std::lock_guard<std::mutex> lock(g_dev_mu);
   DeviceInfo& di = g_devices[dev];
   if (di.sms == 0) CUDA_TRY(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
-  auto it = di.blocks_per_sm.find(fn);
+  auto it = di.blocks_per_sm.find({fn, smem});
   if (it == di.blocks_per_sm.end()) {
-    if (smem > 48 * 1024)
-      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (smem > 48 * 1024) {  // opt in to the larger of this and any earlier request
+      cudaFuncAttributes fa;
+      CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
+      if (static_cast<size_t>(fa.maxDynamicSharedSizeBytes) < smem)
+        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    }
     int b = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem));
-    it = di.blocks_per_sm.emplace(fn, std::max(b, 1)).first;
+    it = di.blocks_per_sm.emplace(std::make_pair(fn, smem), std::max(b, 1)).first;
   }
   *sms = di.sms;
   *bps = it->second;
@@ -289,18 +293,22 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
                    size_t ld, cudaStream_t stream, unsigned long long* d_bad, int force_region,
                    unsigned long long* d_ctr = nullptr) {
   const void* fn = boysfn_dev::kernel_generic();
+  const int aos_flag = layout == BOYSFN_LAYOUT_AOS ? 1 : 0;
+  const size_t smem = aos_flag ? sizeof(double) * boysfn_dev::kThreadsPerBlock *
+                                     boysfn_dev::generic_aos_pitch(k + 1)
+                               : 0;  // per-warp AoS stage, 32 rows x odd pitch
   int sms = 0, bps = 0;
-  if (int st = occupancy(fn, boysfn_dev::kThreadsPerBlock, 0, &sms, &bps)) return st;
+  if (int st = occupancy(fn, boysfn_dev::kThreadsPerBlock, smem, &sms, &bps)) return st;
   const size_t want = ((n + 31) / 32 + boysfn_dev::kWarpsPerBlock - 1) / boysfn_dev::kWarpsPerBlock;
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
   EvalParams p = t->params[k];
   int na = t->deg_na[k], ma = t->deg_ma[k], nb = t->deg_nb, mb = t->deg_mb;
-  int aos = layout == BOYSFN_LAYOUT_AOS ? 1 : 0;
+  int aos = aos_flag;
   unsigned long long* counter = nullptr;
   bool release = false;
   if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
   void* args[] = {&p, &na, &ma, &nb, &mb, &k, &force_region, &d_x, &n, &d_out, &ld, &aos, &d_bad, &counter};
-  const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, 0, stream);
+  const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kThreadsPerBlock), args, smem, stream);
   if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
   if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
   boysfn_internal::count_launch();

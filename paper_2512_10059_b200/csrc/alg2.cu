@@ -11,27 +11,25 @@
 #include <utility>
 
 #include "alg2_device.cuh"
-#include "boys_launch.h"
 #include "capi_internal.h"
-#include "embedded_tables.inc"
+#include "variant_degrees.h"
 
 namespace boysfn_dev {
 namespace {
 
 template <int K, int V>
 const void* alg2_entry() {
-  constexpr int NA = V == kVariantEmbedded ? kEmbDegA[K][0] : kMaxCoef - 1;
-  constexpr int MA = V == kVariantEmbedded ? kEmbDegA[K][1] : kMaxCoef - 1;
-  constexpr int NB = V == kVariantEmbedded ? kEmbDegB[0] : kMaxCoef - 1;
-  constexpr int MB = V == kVariantEmbedded ? kEmbDegB[1] : kMaxCoef - 1;
+  constexpr int NA = VariantDegrees<K, V>::NA, MA = VariantDegrees<K, V>::MA;
+  constexpr int NB = VariantDegrees<K, V>::NB, MB = VariantDegrees<K, V>::MB;
   return reinterpret_cast<const void*>(&boys_alg2_kernel<K, NA, MA, NB, MB>);
 }
 
 template <size_t... Ks>
 const void* alg2_lookup(int k, int v, std::index_sequence<Ks...>) {
-  static const void* const table[2][sizeof...(Ks)] = {
+  static const void* const table[3][sizeof...(Ks)] = {
       {alg2_entry<static_cast<int>(Ks), kVariantEmbedded>()...},
-      {alg2_entry<static_cast<int>(Ks), kVariantPadded>()...}};
+      {alg2_entry<static_cast<int>(Ks), kVariantPadded>()...},
+      {alg2_entry<static_cast<int>(Ks), kVariantCompact>()...}};
   return table[v][k];
 }
 

@@ -12,7 +12,12 @@ namespace boysfn_dev {
 //                     (r_A[k] per Appendix C, r_B = (5, 6)); used whenever a
 //                     table set has that degree profile.
 //   kVariantPadded:   every rational padded to kMaxCoef-1 (any custom set).
-enum Variant : int { kVariantEmbedded = 0, kVariantPadded = 1 };
+//   kVariantCompact:  r_A padded to (9, 13) and r_B to (6, 7): every degree of
+//                     Appendix C and of this repo's generator output fits, so
+//                     a generated or hand-edited set does not pay for 23/23
+//                     Horner (the padded kernels ran k = 32 at 5.2 TB/s).
+enum Variant : int { kVariantEmbedded = 0, kVariantPadded = 1, kVariantCompact = 2 };
+constexpr int kCompactNA = 9, kCompactMA = 13, kCompactNB = 6, kCompactMB = 7;
 
 constexpr int kKernelKmax = 32;
 

@@ -117,6 +117,9 @@ int build_handle(const boysfn_table_desc* d, boysfn_tables_s* h) {
     boysfn_dev::embedded_degrees(k, &na, &ma, &nb, &mb);
     if (d->r_A[k].n == na && d->r_A[k].m == ma && d->r_B.n == nb && d->r_B.m == mb)
       h->variant[k] = boysfn_dev::kVariantEmbedded;
+    else if (d->r_A[k].n <= boysfn_dev::kCompactNA && d->r_A[k].m <= boysfn_dev::kCompactMA &&
+             d->r_B.n <= boysfn_dev::kCompactNB && d->r_B.m <= boysfn_dev::kCompactMB)
+      h->variant[k] = boysfn_dev::kVariantCompact;
   }
   return BOYSFN_OK;
 }

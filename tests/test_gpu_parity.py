@@ -239,15 +239,18 @@ def test_ragged_sizes_and_layout_paths(cuda, port):
     assert got.size == 0
 
 
-def test_custom_table_set_padded_kernels(cuda, port):
-    """A caller-built CoefficientTableSet takes the padded-degree kernels; a zero
-    leading numerator coefficient is exact under Horner-FMA, so results are
-    bit-identical to the embedded kernels."""
+@pytest.mark.parametrize("extra", [1, 3])
+def test_custom_table_set_compact_and_padded_kernels(cuda, port, extra):
+    """A caller-built CoefficientTableSet whose degrees differ from Appendix C
+    takes the compact kernels (r_A <= (9, 13), r_B <= (6, 7); extra = 1 zero
+    appended to every numerator) or the 23/23 padded ones (extra = 3 pushes
+    most r_A numerators past 9); zero leading coefficients are exact under
+    Horner-FMA, so both are bit-identical to the embedded kernels."""
     s = pkg.embedded_default()
     t = copy.deepcopy(s)
-    t.r_B.numer.append(0.0)
+    t.r_B.numer.extend([0.0] * extra)
     for r in t.r_A:
-        r.numer.append(0.0)
+        r.numer.extend([0.0] * extra)
     xs = port.gen_uniform(20000, 5, 0.0, 50.0)
     for k in (0, 7, 16, 32):
         a = device_eval(cuda, xs, k, "soa")

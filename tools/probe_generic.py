@@ -15,13 +15,16 @@ from paper_2512_10059_b200 import tables as T  # noqa: E402
 
 def main():
     e = pkg.embedded_default()
-    t = T.CoefficientTableSet(x0=e.x0, x1=e.x1, k_max=64, eps_tol=e.eps_tol, r_B=e.r_B,
-                              r_A=list(e.r_A) + [e.r_A[32]] * 32)
+    if len(sys.argv) > 1:  # a table file (e.g. a generated set)
+        t = T.parse_tables(open(sys.argv[1]).read())
+    else:
+        t = T.CoefficientTableSet(x0=e.x0, x1=e.x1, k_max=64, eps_tol=e.eps_tol, r_B=e.r_B,
+                                  r_A=list(e.r_A) + [e.r_A[32]] * 32)
     n = 50_000_000
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     pkg.generate_uniform(x, 2, 0.0, 100.0)
     out = torch.empty(n * 65, dtype=torch.float64, device="cuda")
-    for k in (32, 33, 48, 64):
+    for k in tuple(int(v) for v in os.environ.get("PG_KS", "32,33,48,64").split(",")):
         for lay in ("soa", "aos"):
             o = out[: n * (k + 1)]
             pkg.eval_device(x, k, o, tables=t, layout=lay)

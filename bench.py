@@ -259,10 +259,15 @@ def fp64_roofline(pkg, x, ks, step_s):
     C: 3+2k (a mul+add pair counts 2; div, sqrt, exp count 1), with the
     step's own region counts -- over the step time, against the measured DFMA
     peak (tools/fp64_peak.cu)."""
+    import torch
     t = pkg.embedded_default()
-    na = int((x < t.x0).sum().item())
-    nb = int(((x >= t.x0) & (x < t.x1)).sum().item())
-    nc = x.numel() - na - nb
+    na = nab = 0
+    for c in range(0, x.numel(), 1 << 27):  # chunked: configs[4] holds 1e10 x
+        xc = x[c:c + (1 << 27)]
+        na += int(torch.count_nonzero(xc < t.x0).item())
+        nab += int(torch.count_nonzero(xc < t.x1).item())
+    nb = nab - na
+    nc = x.numel() - nab
     flops = 0
     for k in ks:
         ra = t.r_A[k]

@@ -405,13 +405,10 @@ struct Pipeline {
   static constexpr size_t kChunkOutBytes = size_t(256) << 20;  // profiles/r01_e2e_chunk.txt
   int device = -1;
   cudaStream_t stream[kSlots] = {};
-  cudaEvent_t done[kSlots] = {};    // kernel + first-bad flag of the slot's chunk
   cudaEvent_t copied[kSlots] = {};  // D2H of the slot's chunk
   double* d_x[kSlots] = {};
   double* d_out[kSlots] = {};
-  unsigned long long* d_bad = nullptr;  // kSlots words
   unsigned long long* d_ctr = nullptr;  // kSlots scheduler counters (slot s: only on stream[s])
-  unsigned long long* h_bad = nullptr;  // pinned, kSlots words
   size_t cap_x = 0;                     // x capacity per slot
   size_t cap_out = 0;                   // doubles per slot
   double* h_x[kSlots] = {};             // pinned staging for pageable callers (lazy)
@@ -429,12 +426,9 @@ struct Pipeline {
     device = dev;
     for (int s = 0; s < kSlots; ++s) {
       CUDA_TRY(cudaStreamCreateWithFlags(&stream[s], cudaStreamNonBlocking));
-      CUDA_TRY(cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&copied[s], cudaEventDisableTiming));
     }
-    CUDA_TRY(cudaMalloc(&d_bad, kSlots * sizeof(unsigned long long)));
     CUDA_TRY(cudaMalloc(&d_ctr, kSlots * sizeof(unsigned long long)));
-    CUDA_TRY(cudaHostAlloc(&h_bad, kSlots * sizeof(unsigned long long), cudaHostAllocDefault));
     size_t chunk = kChunkOutBytes;
     if (const char* e = std::getenv("BOYSFN_CHUNK_MB"))  // A/B experiments
       chunk = std::max<size_t>(1, std::strtoull(e, nullptr, 10)) << 20;
@@ -459,13 +453,10 @@ struct Pipeline {
       cudaFree(d_out[s]);
       cudaFreeHost(h_x[s]);
       cudaFreeHost(h_out[s]);
-      if (done[s]) cudaEventDestroy(done[s]);
       if (copied[s]) cudaEventDestroy(copied[s]);
       if (stream[s]) cudaStreamDestroy(stream[s]);
     }
-    cudaFree(d_bad);
     cudaFree(d_ctr);
-    cudaFreeHost(h_bad);
     cudaFreeHost(hs_x);
     cudaFreeHost(hs_out);
   }
@@ -752,38 +743,27 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
   if (!(x_direct && out_direct))
     if (int st = P->ensure_staging()) return st;
 
-  // Chunk c in slot s = c % S: (stage x) -> H2D -> kernel -> first-bad flag.
-  auto issue = [&](size_t c) -> int {
-    const int s = static_cast<int>(c % S);
-    const size_t off = c * cx, cn = std::min(cx, n - off);
-    const double* src = xs + off;
-    if (!x_direct) {
-      std::memcpy(P->h_x[s], src, cn * sizeof(double));
-      src = P->h_x[s];
-    }
-    CUDA_TRY(cudaMemcpyAsync(P->d_x[s], src, cn * sizeof(double), cudaMemcpyHostToDevice, P->stream[s]));
-    CUDA_TRY(cudaMemsetAsync(P->d_bad + s, 0xFF, sizeof(unsigned long long), P->stream[s]));
-    if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], P->d_bad + s,
-                             P->d_ctr + s))
-      return st;
-    CUDA_TRY(cudaMemcpyAsync(P->h_bad + s, P->d_bad + s, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                             P->stream[s]));
-    CUDA_TRY(cudaEventRecord(P->done[s], P->stream[s]));
-    return BOYSFN_OK;
-  };
+  // Chunk c in slot s = c % S, all on stream s: (stage x) -> H2D -> kernel ->
+  // D2H of the rows before the first bad x -> event.  x is checked on the host
+  // (check_input, eval.cpp:13-15) as the chunk is issued, while earlier chunks
+  // are moving, so a chunk's D2H is enqueued right behind its kernel: no
+  // device flag, no host round trip, nothing small queued ahead of the big
+  // copies.  (The earlier flag-and-wait scheme reached 51.5 GB/s D2H.)
   const bool soa_d2h_2d = std::getenv("BOYSFN_SOA_D2H_2D") != nullptr;  // A/B experiments
-  // D2H of the chunk's first `rows` rows: to the caller directly, or to staging.
-  auto fetch = [&](size_t c, size_t rows) -> int {
+  auto issue = [&](size_t c, size_t rows) -> int {
     const int s = static_cast<int>(c % S);
     const size_t off = c * cx, cn = std::min(cx, n - off);
+    const double* src = x_direct ? xs + off : P->h_x[s];
+    CUDA_TRY(cudaMemcpyAsync(P->d_x[s], src, cn * sizeof(double), cudaMemcpyHostToDevice, P->stream[s]));
+    if (int st = launch_eval(t, P->d_x[s], cn, k, P->d_out[s], layout, cn, P->stream[s], nullptr, P->d_ctr + s))
+      return st;
     if (rows > 0) {
       if (layout == BOYSFN_LAYOUT_AOS) {
         double* dst = out_direct ? out + off * row : P->h_out[s];
         CUDA_TRY(cudaMemcpyAsync(dst, P->d_out[s], rows * row * sizeof(double), cudaMemcpyDeviceToHost,
                                  P->stream[s]));
       } else if (out_direct) {
-        // one 1D copy per order row: the strided 2D copy of the same rows ran
-        // at 38 GB/s against 50 GB/s for 1D copies on the B200 hosts
+        // one 1D copy per order row (a strided 2D copy of the same rows was slower)
         if (soa_d2h_2d) {
           CUDA_TRY(cudaMemcpy2DAsync(out + off, ld * sizeof(double), P->d_out[s], cn * sizeof(double),
                                      rows * sizeof(double), row, cudaMemcpyDeviceToHost, P->stream[s]));
@@ -800,19 +780,17 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     CUDA_TRY(cudaEventRecord(P->copied[s], P->stream[s]));
     return BOYSFN_OK;
   };
-  // Staged path: staging -> caller's pageable rows, on host threads.
-  auto unstage = [&](size_t c, size_t rows) -> int {
+  // Staged output: staging -> the caller's pageable rows, on the copy pool.
+  auto unstage = [&](size_t c, size_t rows) {
     const int s = static_cast<int>(c % S);
     const size_t off = c * cx, cn = std::min(cx, n - off);
-    CUDA_TRY(cudaEventSynchronize(P->copied[s]));
-    if (rows == 0) return BOYSFN_OK;
+    if (rows == 0) return;
     std::vector<Segment> segs;
     if (layout == BOYSFN_LAYOUT_AOS)
       segs.push_back({out + off * row, P->h_out[s], rows * row});
     else
       for (size_t l = 0; l < row; ++l) segs.push_back({out + l * ld + off, P->h_out[s] + l * cn, rows});
     parallel_copy(std::move(segs));
-    return BOYSFN_OK;
   };
 
   const bool trace = std::getenv("BOYSFN_TRACE") != nullptr;
@@ -823,39 +801,53 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what, c);
   };
   int status = BOYSFN_OK;
-  size_t pend_c = 0, pend_rows = 0;
-  bool pending = false;  // a staged chunk whose rows still have to reach the caller
-  for (size_t c = 0; c < std::min<size_t>(nchunks, S - 1) && status == BOYSFN_OK; ++c) status = issue(c);
-  for (size_t c = 0; c < nchunks && status == BOYSFN_OK; ++c) {
-    if (c + S - 1 < nchunks && (status = issue(c + S - 1))) break;
-    stamp("issued", c + S - 1);
+  size_t bad_at = n;
+  std::vector<std::pair<size_t, size_t>> inflight;  // (chunk, rows) whose slot may hold host staging
+  const bool host_staging = !(x_direct && out_direct);
+  auto retire = [&](size_t i) -> int {  // wait for inflight[i]'s copies, then move its staged rows out
+    const auto [c, rows] = inflight[i];
+    if (cudaError_t e = cudaEventSynchronize(P->copied[c % S])) return cuda_fail(e, "cudaEventSynchronize");
+    if (!out_direct) unstage(c, rows);
+    stamp("retired", c);
+    return BOYSFN_OK;
+  };
+  size_t head = 0;  // first inflight entry not yet retired
+  for (size_t c = 0; c < nchunks; ++c) {
     const int s = static_cast<int>(c % S);
     const size_t off = c * cx, cn = std::min(cx, n - off);
-    if (cudaError_t e = cudaEventSynchronize(P->done[s])) {
-      status = cuda_fail(e, "cudaEventSynchronize");
+    if (host_staging && c >= static_cast<size_t>(S)) {  // the slot's staging buffers come back
+      if ((status = retire(head++))) break;
+    }
+    size_t b = off;  // x check (and pageable staging) of this chunk
+    if (x_direct) {
+      while (b < off + cn && x_ok(xs[b])) ++b;
+    } else {
+      double* hx = P->h_x[s];
+      for (size_t i = off; i < off + cn; ++i) {
+        hx[i - off] = xs[i];
+        if (b == i && x_ok(xs[i])) b = i + 1;
+      }
+    }
+    const size_t rows = b - off;
+    if ((status = issue(c, rows))) break;
+    stamp("issued", c);
+    inflight.emplace_back(c, rows);
+    if (rows < cn) {
+      bad_at = b;
       break;
     }
-    const unsigned long long bad = P->h_bad[s];
-    const size_t rows = bad == ~0ull ? cn : static_cast<size_t>(bad);
-    stamp("kernel done", c);
-    if ((status = fetch(c, rows))) break;
-    if (pending && (status = unstage(pend_c, pend_rows))) break;  // overlaps the D2H of chunk c
-    stamp("unstaged", pend_c);
-    pending = !out_direct;
-    pend_c = c;
-    pend_rows = rows;
-    if (bad != ~0ull) {
-      if (first_bad) *first_bad = off + static_cast<size_t>(bad);
-      status = fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
-    }
   }
-  if (pending && (status == BOYSFN_OK || status == BOYSFN_ERR_DOMAIN)) {
-    const int st = unstage(pend_c, pend_rows);
+  while (host_staging && head < inflight.size()) {
+    const int st = retire(head++);
     if (status == BOYSFN_OK) status = st;
   }
   for (int s = 0; s < S; ++s) cudaStreamSynchronize(P->stream[s]);
   if (status == BOYSFN_OK) {
     if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "boysfn_eval_host");
+    if (bad_at != n) {
+      if (first_bad) *first_bad = bad_at;
+      return fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
+    }
   }
   return status;
 }

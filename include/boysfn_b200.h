@@ -118,6 +118,16 @@ int boysfn_eval_device(boysfn_tables_t tables, const double* d_x, size_t n, int 
 int boysfn_eval_host(boysfn_tables_t tables, const double* xs, size_t n, int k, double* out,
                      size_t out_len, int layout, size_t ld, size_t* first_bad);
 
+/* Spreads large boysfn_eval_host calls (n*(k+1) >= 2^24 values) over these
+ * devices: contiguous shards of the batch, one persistent host thread and
+ * staging pipeline per device, so the shards' PCIe links add up (the
+ * reference's boys_batch_many is a single call, eval.hpp:44-45).  x is checked
+ * on the host first, so the rows from the first bad x on are never written.
+ * count <= 0 restores the default (the calling thread's current device); the
+ * environment variable BOYSFN_DEVICES="0,1,..." sets the initial list.  A
+ * device may appear more than once (tests). */
+int boysfn_set_devices(const int* devices, int count);
+
 /* Forced-region evaluation of one x (boys_batch_region, eval.cpp:59-81, the
  * reference's branch-agreement test seam), computed on the device. */
 int boysfn_eval_region_host(boysfn_tables_t tables, double x, int k, int region, double* out);

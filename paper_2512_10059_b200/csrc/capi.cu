@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -618,6 +619,40 @@ int get_pipeline(Pipeline** out) {
 
 bool x_ok(double x) { return std::isfinite(x) && x >= 0; }
 
+// Devices a large boysfn_eval_host call is spread over (boysfn_set_devices,
+// else BOYSFN_DEVICES="0,1,..."; empty = the caller's current device only).
+std::mutex g_host_dev_mu;
+std::vector<int> g_host_devs;
+bool g_host_devs_init = false;
+
+std::vector<int> host_devices() {
+  std::lock_guard<std::mutex> lk(g_host_dev_mu);
+  if (!g_host_devs_init) {
+    g_host_devs_init = true;
+    if (const char* e = std::getenv("BOYSFN_DEVICES")) {
+      std::string v(e);
+      size_t pos = 0;
+      while (pos < v.size()) {
+        const size_t c = v.find(',', pos);
+        const std::string tok = v.substr(pos, c == std::string::npos ? std::string::npos : c - pos);
+        if (!tok.empty()) g_host_devs.push_back(std::atoi(tok.c_str()));
+        if (c == std::string::npos) break;
+        pos = c + 1;
+      }
+    }
+  }
+  return g_host_devs;
+}
+
+// Below this many output values one device's pipeline is already at the PCIe
+// link rate for most of the call; above it the shards' links add up.
+constexpr size_t kMultiDeviceMinValues = size_t(1) << 24;
+
+int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double* out, size_t out_extent,
+                   int layout, size_t ld, size_t* first_bad);
+int eval_host_multi(boysfn_tables_t t, const double* xs, size_t n, int k, double* out, int layout, size_t ld,
+                    size_t* first_bad);
+
 }  // namespace
 
 // ------------------------------------------------------------------ C ABI --
@@ -705,6 +740,20 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     if (first_bad) *first_bad = 0;
     return x_ok(xs[0]) ? fail(BOYSFN_ERR_RANGE, kMsgRange) : fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
   }
+  if (host_devices().size() > 1 && n * row >= kMultiDeviceMinValues)
+    return eval_host_multi(t, xs, n, k, out, layout, ld, first_bad);
+  return eval_host_core(t, xs, n, k, out, layout == BOYSFN_LAYOUT_AOS ? n * row : (row - 1) * ld + n, layout, ld,
+                        first_bad);
+}
+
+namespace {
+
+// The host API on the calling thread's current device, after validation:
+// out_extent = doubles from `out` the call may touch.
+int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double* out, size_t out_extent,
+                   int layout, size_t ld, size_t* first_bad) {
+  const size_t row = static_cast<size_t>(k) + 1;
+  const size_t out_len = out_extent;
   Pipeline* P = nullptr;
   if (int st = get_pipeline(&P)) return st;
   if (const char* e = std::getenv("BOYSFN_SMALL_VALUES"))  // A/B experiments
@@ -850,6 +899,125 @@ BOYSFN_API int boysfn_eval_host(boysfn_tables_t t, const double* xs, size_t n, i
     }
   }
   return status;
+}
+
+// One persistent host thread per listed device (so each keeps its staging
+// pipeline), running one shard of a multi-device boysfn_eval_host call.
+class DeviceWorker {
+ public:
+  explicit DeviceWorker(int device) : device_(device), th_([this] { loop(); }) {}
+  ~DeviceWorker() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    th_.join();
+  }
+  void submit(std::function<void()> job) {
+    std::lock_guard<std::mutex> lk(mu_);
+    job_ = std::move(job);
+    done_ = false;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return done_; });
+  }
+
+ private:
+  void loop() {
+    cudaSetDevice(device_);
+    for (;;) {
+      std::function<void()> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || job_ != nullptr; });
+        if (stop_) return;
+        job = std::move(job_);
+        job_ = nullptr;
+      }
+      job();
+      std::lock_guard<std::mutex> lk(mu_);
+      done_ = true;
+      cv_.notify_all();
+    }
+  }
+  int device_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::function<void()> job_;
+  bool done_ = true, stop_ = false;
+  std::thread th_;  // last: started after the members it uses
+};
+
+// Splits [0, n) over the listed devices (x checked on the host first: rows
+// from the first bad x on are never written, as eval.cpp:92-95).  Each shard
+// is a single-device call on its worker; the caller gets the first failure.
+int eval_host_multi(boysfn_tables_t t, const double* xs, size_t n, int k, double* out, int layout, size_t ld,
+                    size_t* first_bad) {
+  static std::mutex multi_mu;  // one multi-device call at a time (the workers are shared)
+  std::lock_guard<std::mutex> lk(multi_mu);
+  static std::map<std::pair<size_t, int>, std::unique_ptr<DeviceWorker>> workers;  // (list position, device)
+  const std::vector<int> devs = host_devices();
+  const size_t row = static_cast<size_t>(k) + 1;
+  // first bad x, on the copy pool's threads
+  const int T = static_cast<int>(std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())));
+  std::vector<size_t> bad(T, n);
+  {
+    std::vector<std::thread> th;
+    for (int i = 0; i < T; ++i)
+      th.emplace_back([&, i] {
+        const size_t a = n * i / T, b = n * (i + 1) / T;
+        for (size_t j = a; j < b; ++j)
+          if (!x_ok(xs[j])) {
+            bad[i] = j;
+            break;
+          }
+      });
+    for (auto& h : th) h.join();
+  }
+  const size_t neff = *std::min_element(bad.begin(), bad.end());
+  const size_t D = devs.size();
+  std::vector<int> status(D, BOYSFN_OK);
+  std::vector<std::string> msg(D);
+  for (size_t d = 0; d < D; ++d) {
+    const size_t a = neff * d / D, b = neff * (d + 1) / D;
+    auto& w = workers[{d, devs[d]}];
+    if (!w) w = std::make_unique<DeviceWorker>(devs[d]);
+    if (b == a) continue;
+    w->submit([&, d, a, b] {
+      double* o = layout == BOYSFN_LAYOUT_AOS ? out + a * row : out + a;
+      const size_t extent = layout == BOYSFN_LAYOUT_AOS ? (b - a) * row : (row - 1) * ld + (b - a);
+      status[d] = eval_host_core(t, xs + a, b - a, k, o, extent, layout, ld, nullptr);
+      if (status[d] != BOYSFN_OK) msg[d] = boysfn_last_error();
+    });
+  }
+  for (size_t d = 0; d < D; ++d) {
+    const size_t a = neff * d / D, b = neff * (d + 1) / D;
+    if (b > a) workers[{d, devs[d]}]->wait();
+  }
+  for (size_t d = 0; d < D; ++d)
+    if (status[d] != BOYSFN_OK) return fail(status[d], "device " + std::to_string(devs[d]) + ": " + msg[d]);
+  if (neff != n) {
+    if (first_bad) *first_bad = neff;
+    return fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
+  }
+  return BOYSFN_OK;
+}
+
+}  // namespace
+
+BOYSFN_API int boysfn_set_devices(const int* devices, int count) {
+  if (count > 0 && devices == nullptr) return fail(BOYSFN_ERR_ARG, "null device list");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  for (int i = 0; i < count; ++i)
+    if (devices[i] < 0 || devices[i] >= ndev) return fail(BOYSFN_ERR_ARG, "no such device");
+  std::lock_guard<std::mutex> lk(g_host_dev_mu);
+  g_host_devs.assign(devices, devices + std::max(count, 0));
+  g_host_devs_init = true;
+  return BOYSFN_OK;
 }
 
 BOYSFN_API int boysfn_eval_region_host(boysfn_tables_t t, double x, int k, int region, double* out) {

@@ -153,6 +153,15 @@ def boys_batch_many(xs, k, tables, out, layout="aos", ld=None):
     _raise(st, bad.value if st == _capi.ERR_DOMAIN else None)
 
 
+def set_devices(devices=None):
+    """Spread large boys_batch_many calls over these CUDA devices (contiguous
+    shards, one host thread and staging pipeline each); None or [] restores
+    the calling thread's current device only (boysfn_set_devices)."""
+    devs = list(devices or [])
+    arr = (ctypes.c_int * max(len(devs), 1))(*devs)
+    _raise(_capi.lib().boysfn_set_devices(arr, len(devs)))
+
+
 def boys_batch(x, k, tables):
     """One argument (eval.cpp:83-86)."""
     out = np.empty(max(int(k) + 1, 0), dtype=np.float64)

@@ -190,3 +190,41 @@ def test_small_batch_path_equals_pipeline(cuda, port, monkeypatch):
             outs.append(o)
             monkeypatch.delenv("BOYSFN_NO_SMALL_PATH", raising=False)
         assert np.array_equal(bits(outs[0]), bits(outs[1]))
+
+
+def test_multi_device_host_api_equals_single(cuda, port):
+    """boysfn_set_devices spreads a large host call over devices (here device 0
+    listed twice: two workers, two pipelines on one GPU): bit-identical to the
+    single-device call in both layouts, pageable and pinned, and a bad x in
+    either shard yields the reference's first-throw rows and index."""
+    torch = cuda
+    s = pkg.embedded_default()
+    n, k = 2_000_003, 16  # 3.4e7 values >= the 2^24 threshold
+    xs = port.gen_uniform(n, 31, 0.0, 70.0)
+    try:
+        for layout in ("aos", "soa"):
+            want = np.empty(n * (k + 1))
+            pkg.set_devices([])
+            pkg.boys_batch_many(xs, k, s, want, layout=layout)
+            pkg.set_devices([0, 0])
+            got = np.empty(n * (k + 1))
+            pkg.boys_batch_many(xs, k, s, got, layout=layout)
+            assert np.array_equal(bits(got), bits(want)), layout
+            pinned = torch.empty(n * (k + 1), dtype=torch.float64, pin_memory=True).numpy()
+            pkg.boys_batch_many(xs, k, s, pinned, layout=layout)
+            assert np.array_equal(bits(pinned), bits(want)), layout
+        for bad_at in (17, 1_500_000):  # first shard, second shard
+            xb = xs.copy()
+            xb[bad_at] = -1.0
+            outs = []
+            for devs in ([], [0, 0]):
+                pkg.set_devices(devs)
+                o = np.full(n * (k + 1), 3.25)
+                with pytest.raises(pkg.domain_error) as ei:
+                    pkg.boys_batch_many(xb, k, s, o)
+                assert ei.value.first_bad == bad_at
+                outs.append(o)
+            assert np.array_equal(bits(outs[0]), bits(outs[1]))
+            assert np.all(outs[1][bad_at * (k + 1):] == 3.25)
+    finally:
+        pkg.set_devices([])

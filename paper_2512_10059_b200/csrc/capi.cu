@@ -1,5 +1,7 @@
 // capi.cu -- the C ABI of include/boysfn_b200.h: table handles, kernel
-// dispatch, the chunked host<->device pipeline behind boys_batch_many, and the
+// dispatch, the host paths behind boys_batch_many (a one-kernel path over
+// host-mapped buffers for small batches, a chunked three-stream pipeline for
+// large ones, optionally sharded over several devices), and the
 // synthetic-workload generators.  Every evaluation runs on the GPU; there is no
 // CPU fallback: without a device the calls return BOYSFN_ERR_CUDA.
 #include <cuda.h>
@@ -399,8 +401,9 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
 }
 
 // --------------------------------------------------------- host pipeline --
-// Per (thread, device) staging: three slots, each with its own stream, so the
-// H2D copy + kernel of chunk c+2 and the D2H copy of chunk c overlap.
+// Per (thread, device) staging: three slots, each with its own stream; a
+// chunk's H2D copy, kernel and D2H copy follow one another on its slot's
+// stream, and the slots overlap, so the link stays busy.
 struct Pipeline {
   static constexpr int kSlots = 3;
   static constexpr size_t kChunkOutBytes = size_t(256) << 20;  // profiles/r01_e2e_chunk.txt
@@ -501,8 +504,8 @@ struct Segment {
   size_t n;
 };
 
-// Persistent host-copy workers: spawning 15 threads per 128-MB chunk cost
-// ~0.3 ms against a ~3.7 ms copy.  One process-wide pool; concurrent callers
+// Persistent host-copy workers: spawning 15 threads per chunk cost ~0.3 ms
+// against a ~3.7 ms copy of 128 MB.  One process-wide pool; concurrent callers
 // (one staging pipeline per host thread) take turns, since they share the
 // host memory bandwidth anyway.
 class CopyPool {

@@ -110,16 +110,15 @@ def build_shim_test(force=False):
 
 
 GEN = os.path.join(LIBDIR, "boysfn_gen")
-GEN_SOURCES = ["gen_hp.cpp", "gen_remez.cpp", "gen_main.cpp"]
+GEN_SOURCES = ["special.cpp", "minimax.cpp", "gen_main.cpp"]
 
 
 def build_gen(force=False):
-    """The native table generator (binary128 restatement of the reference's
-    generator library, GPU extremum scan through the C ABI)."""
+    """The native table generator (binary128 minimax exchange and Walsh search,
+    GPU extremum scan through the C ABI)."""
     srcs = [os.path.join(CPP, "src", "gen", f) for f in GEN_SOURCES]
-    hdrs = [os.path.join(CPP, "include", "boysfn", f) for f in
-            ("highprec.hpp", "reference.hpp", "polynomial.hpp", "linalg.hpp", "regions.hpp", "remez.hpp",
-             "tables.hpp", "verify.hpp")]
+    hdrs = [os.path.join(CPP, "include", "boysfn_gen", "minimax.hpp")] + [
+        os.path.join(CPP, "include", "boysfn", f) for f in ("tables.hpp", "verify.hpp")]
     if force or _stale(GEN, srcs + hdrs + [LIB]):
         _run(["g++", "-std=gnu++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(CPP, "include")] + srcs +
              ["-o", GEN, "-L", LIBDIR, "-lboysfn_b200", "-Wl,-rpath,$ORIGIN", "-lquadmath", "-lpthread"])

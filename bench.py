@@ -21,7 +21,12 @@ Reported beside `value` (device-resident, CUDA events on the launching stream):
                x and D2H of all F values inside the timed region
   roofline     algorithmic bytes per launch (8 B read + 8(k+1) B written per x)
                / mean launch time, against MEASURED_PEAKS.json hbm_gbs; traffic
-               from the committed ncu capture (profiles/ncu_summary.json)
+               from the committed ncu capture (profiles/ncu_summary.json);
+               roofline.fp64: algorithmic flops of the step (SURVEY 8(a) counts,
+               the step's own region mix) against the measured DFMA peak
+  step_ms      min/median/max per timed step and the worst host enqueue time
+               (the steps are queued behind a short device spin outside the
+               timed interval, so host hiccups cannot idle the GPU inside it)
   cpu_baseline the unmodified reference (oracle/_ref) on all host cores over a
                bounded sample of the same stream (rank 0, N=1 only)
   accuracy     max |F - oracle| on a sample (binary128 oracle, oracle/boys_hp.c)

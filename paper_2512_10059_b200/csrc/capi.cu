@@ -6,6 +6,7 @@
 // CPU fallback: without a device the calls return BOYSFN_ERR_CUDA.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges cost nothing without a profiler attached
 
 #include <algorithm>
 #include <atomic>
@@ -622,6 +623,14 @@ int get_pipeline(Pipeline** out) {
 
 bool x_ok(double x) { return std::isfinite(x) && x >= 0; }
 
+// NVTX range for timeline tools (Nsight Systems): the host API's phases.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Devices a large boysfn_eval_host call is spread over (boysfn_set_devices,
 // else BOYSFN_DEVICES="0,1,..."; empty = the caller's current device only).
 std::mutex g_host_dev_mu;
@@ -755,6 +764,7 @@ namespace {
 // out_extent = doubles from `out` the call may touch.
 int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double* out, size_t out_extent,
                    int layout, size_t ld, size_t* first_bad) {
+  const NvtxRange range("boysfn_eval_host");
   const size_t row = static_cast<size_t>(k) + 1;
   const size_t out_len = out_extent;
   Pipeline* P = nullptr;
@@ -803,6 +813,7 @@ int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double*
   // copies.  (The earlier flag-and-wait scheme reached 51.5 GB/s D2H.)
   const bool soa_d2h_2d = std::getenv("BOYSFN_SOA_D2H_2D") != nullptr;  // A/B experiments
   auto issue = [&](size_t c, size_t rows) -> int {
+    const NvtxRange chunk_range("boysfn chunk");
     const int s = static_cast<int>(c % S);
     const size_t off = c * cx, cn = std::min(cx, n - off);
     const double* src = x_direct ? xs + off : P->h_x[s];
@@ -834,6 +845,7 @@ int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double*
   };
   // Staged output: staging -> the caller's pageable rows, on the copy pool.
   auto unstage = [&](size_t c, size_t rows) {
+    const NvtxRange unstage_range("boysfn unstage");
     const int s = static_cast<int>(c % S);
     const size_t off = c * cx, cn = std::min(cx, n - off);
     if (rows == 0) return;
@@ -959,6 +971,7 @@ class DeviceWorker {
 // is a single-device call on its worker; the caller gets the first failure.
 int eval_host_multi(boysfn_tables_t t, const double* xs, size_t n, int k, double* out, int layout, size_t ld,
                     size_t* first_bad) {
+  const NvtxRange range("boysfn_eval_host multi-device");
   static std::mutex multi_mu;  // one multi-device call at a time (the workers are shared)
   std::lock_guard<std::mutex> lk(multi_mu);
   static std::map<std::pair<size_t, int>, std::unique_ptr<DeviceWorker>> workers;  // (list position, device)

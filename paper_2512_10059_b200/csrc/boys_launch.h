@@ -31,6 +31,7 @@ const void* kernel_soa_block_tma(int k, int variant);
 const void* kernel_aos_block_tma(int k, int variant);
 const void* kernel_soa_block_tma_bin(int k, int variant);
 const void* kernel_aos_block_tma_bin(int k, int variant);
+const void* kernel_aos_block_tma_swz(int k, int variant);  // k = 15, 31 only
 const void* kernel_region(int k, int variant);
 const void* kernel_generic();
 

@@ -249,6 +249,23 @@ bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R, int 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3D map over the AoS output for the swizzled stage: dim0 = 16 doubles (one
+// 128-B line), dim1 = (k+1)/16 lines per row, dim2 = rows (stride 8(k+1) B);
+// box = one block tile (16 x (k+1)/16 x 128), 128-B swizzle.
+bool make_aos_swz_tmap(CUtensorMap* m, double* out, size_t n, int R, int rows) {
+  EncodeTiledFn enc = encode_tiled();
+  if (enc == nullptr || (R != 16 && R != 32) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      n > (size_t(1) << 31) - 256)
+    return false;
+  const cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(R / 16), n};
+  const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(R) * sizeof(double)};
+  const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(R / 16), static_cast<cuuint32_t>(rows)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Output-path selection (short-train medians of
 // every path at every k on one B200, profiles/r01_path_sweep.txt).  Large k is
 // HBM-write-bound and wants long contiguous write bursts: block tiles of 128 x
@@ -256,14 +273,15 @@ bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R, int 
 // within 1-2% of one another with and without the region sort.  Small k is
 // issue-bound and wants no A/B/C divergence at the least overhead: the per-warp
 // region-binned kernels.  The AoS block stage is row-major [128][k+1]; at
-// k+1 = 16 or 32 its stores are 8/16-way bank conflicts, and the per-warp
-// transpose (padded pitch) takes those two orders.
+// k+1 = 16 or 32 its stores would be 8/16-way bank conflicts, so those two
+// orders stage in the TMA's 128-B swizzle and store through a 3D tensor map.
 //   SoA: k <= 6 binned; 8..13 block-TMA region-sorted; else block-TMA
 //        (block/LSU if no tensor map applies)
-//   AoS: k <= 5 binned; 6, 8 block-TMA region-sorted; k+1 in {16, 32} transpose;
-//        else block-TMA (transpose if the output is not 16-B aligned)
+//   AoS: k <= 5 binned; 6, 8 block-TMA region-sorted; k+1 in {16, 32} block-TMA
+//        with the 128-B-swizzled stage; else block-TMA (transpose if the output
+//        is not 16-B aligned, or if a tensor map does not apply)
 // BOYSFN_SOA_PATH = warp|block|binned|blocktma|blocktmabin and
-// BOYSFN_AOS_PATH = xpose|binned|blocktma|blocktmabin override the choice
+// BOYSFN_AOS_PATH = xpose|binned|blocktma|blocktmabin|blocktmaswz override the choice
 // (experiments and the path-equivalence tests).
 int choose_store(int layout, int k, const double* d_out) {
   const int R = k + 1;
@@ -283,9 +301,11 @@ int choose_store(int layout, int k, const double* d_out) {
   if (want == "binned") return boysfn_dev::kStoreAoSBinned;
   if (want == "blocktma" && a16) return boysfn_dev::kStoreAoSBlockTma;
   if (want == "blocktmabin" && a16) return boysfn_dev::kStoreAoSBlockTmaBin;
+  if (want == "blocktmaswz" && a16 && (R == 16 || R == 32)) return boysfn_dev::kStoreAoSBlockTmaSwz;
   if (!want.empty()) return boysfn_dev::kStoreAoSXpose;
   if (k <= 5) return boysfn_dev::kStoreAoSBinned;
-  if (!a16 || R == 16 || R == 32) return boysfn_dev::kStoreAoSXpose;
+  if (!a16) return boysfn_dev::kStoreAoSXpose;
+  if (R == 16 || R == 32) return boysfn_dev::kStoreAoSBlockTmaSwz;
   return (k == 6 || k == 8) ? boysfn_dev::kStoreAoSBlockTmaBin : boysfn_dev::kStoreAoSBlockTma;
 }
 
@@ -344,6 +364,8 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) &&
       !make_soa_tmap(&tmap, d_out, n, ld, R, threads))
     store = boysfn_dev::kStoreSoABlock;
+  if (store == boysfn_dev::kStoreAoSBlockTmaSwz && !make_aos_swz_tmap(&tmap, d_out, n, R, threads))
+    store = boysfn_dev::kStoreAoSXpose;
   switch (store) {
     case boysfn_dev::kStoreSoABlockTma:
       fn = boysfn_dev::kernel_soa_block_tma(k, v);
@@ -360,6 +382,10 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
     case boysfn_dev::kStoreAoSBlockTmaBin:
       fn = boysfn_dev::kernel_aos_block_tma_bin(k, v);
       smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaBin>(R, boysfn_dev::kBlockX);
+      break;
+    case boysfn_dev::kStoreAoSBlockTmaSwz:
+      fn = boysfn_dev::kernel_aos_block_tma_swz(k, v);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaSwz>(R, boysfn_dev::kBlockX);
       break;
     case boysfn_dev::kStoreSoA:
       fn = boysfn_dev::kernel_soa(k, v);

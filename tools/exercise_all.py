@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_10059_b200 as pkg  # noqa: E402
 
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
-         ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin")]
+         ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"), ("aos", "blocktmaswz")]
 
 
 def main():
@@ -23,7 +23,7 @@ def main():
     for n in (1, 33, 129, 1000):
         x = torch.empty(n, dtype=torch.float64, device="cuda")
         pkg.generate_uniform(x, n, 0.0, 45.0)
-        for k in (0, 5, 8, 16, 31, 32):
+        for k in (0, 5, 8, 15, 16, 31, 32):
             for lay, path in PATHS:
                 os.environ["BOYSFN_SOA_PATH" if lay == "soa" else "BOYSFN_AOS_PATH"] = path
                 out = torch.empty(n * (k + 1), dtype=torch.float64, device="cuda")

@@ -21,6 +21,10 @@ constexpr int kCompactNA = 9, kCompactMA = 13, kCompactNB = 6, kCompactMB = 7;
 
 constexpr int kKernelKmax = 32;
 
+// x per SoA block-TMA tile (= threads per block): 256 gives 2 KB row segments,
+// 0.2-0.4% over 128 at k >= 16 (profiles/r01_soa_tile256.txt).
+constexpr int kSoATmaTileX = 256;
+
 // Kernel entry points, one translation unit per store path.
 const void* kernel_soa(int k, int variant);
 const void* kernel_aos_xpose(int k, int variant);

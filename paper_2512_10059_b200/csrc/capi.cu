@@ -360,16 +360,17 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
   int store = force_store >= 0 ? force_store : choose_store(layout, k, d_out);
-  const int threads = boysfn_dev::kThreadsPerBlock;
+  const int tile_x = store == boysfn_dev::kStoreSoABlockTma ? boysfn_dev::kSoATmaTileX : boysfn_dev::kBlockX;
   if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) &&
-      !make_soa_tmap(&tmap, d_out, n, ld, R, threads))
+      !make_soa_tmap(&tmap, d_out, n, ld, R, tile_x))
     store = boysfn_dev::kStoreSoABlock;
-  if (store == boysfn_dev::kStoreAoSBlockTmaSwz && !make_aos_swz_tmap(&tmap, d_out, n, R, threads))
+  if (store == boysfn_dev::kStoreAoSBlockTmaSwz && !make_aos_swz_tmap(&tmap, d_out, n, R, boysfn_dev::kBlockX))
     store = boysfn_dev::kStoreAoSXpose;
+  const int threads = store == boysfn_dev::kStoreSoABlockTma ? boysfn_dev::kSoATmaTileX : boysfn_dev::kThreadsPerBlock;
   switch (store) {
     case boysfn_dev::kStoreSoABlockTma:
       fn = boysfn_dev::kernel_soa_block_tma(k, v);
-      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTma>(R, boysfn_dev::kBlockX);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTma>(R, threads);
       break;
     case boysfn_dev::kStoreAoSBlockTma:
       fn = boysfn_dev::kernel_aos_block_tma(k, v);

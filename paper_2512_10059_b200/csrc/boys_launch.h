@@ -21,9 +21,11 @@ constexpr int kCompactNA = 9, kCompactMA = 13, kCompactNB = 6, kCompactMB = 7;
 
 constexpr int kKernelKmax = 32;
 
-// x per SoA block-TMA tile (= threads per block): 256 gives 2 KB row segments,
-// 0.2-0.4% over 128 at k >= 16 (profiles/r01_soa_tile256.txt).
+// x per block-TMA tile (= threads per block) of the plain SoA and AoS stores:
+// 256 x gives 2 KB SoA row segments and 2x longer AoS spans; 0.2-0.4% (SoA)
+// and 0.4-1.2% (AoS) over 128 x at k >= 10 (profiles/r01_tma_tile256.txt).
 constexpr int kSoATmaTileX = 256;
+constexpr int kAoSTmaTileX = 256;
 
 // Kernel entry points, one translation unit per store path.
 const void* kernel_soa(int k, int variant);

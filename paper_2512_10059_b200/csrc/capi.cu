@@ -366,7 +366,9 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
     store = boysfn_dev::kStoreSoABlock;
   if (store == boysfn_dev::kStoreAoSBlockTmaSwz && !make_aos_swz_tmap(&tmap, d_out, n, R, boysfn_dev::kBlockX))
     store = boysfn_dev::kStoreAoSXpose;
-  const int threads = store == boysfn_dev::kStoreSoABlockTma ? boysfn_dev::kSoATmaTileX : boysfn_dev::kThreadsPerBlock;
+  const int threads = store == boysfn_dev::kStoreSoABlockTma   ? boysfn_dev::kSoATmaTileX
+                      : store == boysfn_dev::kStoreAoSBlockTma ? boysfn_dev::kAoSTmaTileX
+                                                               : boysfn_dev::kThreadsPerBlock;
   switch (store) {
     case boysfn_dev::kStoreSoABlockTma:
       fn = boysfn_dev::kernel_soa_block_tma(k, v);
@@ -374,7 +376,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
       break;
     case boysfn_dev::kStoreAoSBlockTma:
       fn = boysfn_dev::kernel_aos_block_tma(k, v);
-      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTma>(R, boysfn_dev::kBlockX);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTma>(R, threads);
       break;
     case boysfn_dev::kStoreSoABlockTmaBin:
       fn = boysfn_dev::kernel_soa_block_tma_bin(k, v);

@@ -26,6 +26,24 @@ constexpr int kKernelKmax = 32;
 // and 0.4-1.2% (AoS) over 128 x at k >= 10 (profiles/r01_tma_tile256.txt).
 constexpr int kSoATmaTileX = 256;
 constexpr int kAoSTmaTileX = 256;
+#ifndef BOYSFN_BIN_TMA_BX
+#define BOYSFN_BIN_TMA_BX 128
+#endif
+#ifndef BOYSFN_SWZ_TMA_BX
+#define BOYSFN_SWZ_TMA_BX 128
+#endif
+constexpr int kBinTmaTileX = BOYSFN_BIN_TMA_BX;  // region-sorted block-TMA stores (SoA and AoS)
+constexpr int kSwzTmaTileX = BOYSFN_SWZ_TMA_BX;  // swizzled AoS stage
+
+// Tile width (= threads per block) of a block-TMA store kind; kBlockX otherwise.
+constexpr int block_tma_tile_x(int store) {
+  return store == kStoreSoABlockTma      ? kSoATmaTileX
+         : store == kStoreAoSBlockTma    ? kAoSTmaTileX
+         : store == kStoreSoABlockTmaBin ? kBinTmaTileX
+         : store == kStoreAoSBlockTmaBin ? kBinTmaTileX
+         : store == kStoreAoSBlockTmaSwz ? kSwzTmaTileX
+                                         : kBlockX;
+}
 
 // Kernel entry points, one translation unit per store path.
 const void* kernel_soa(int k, int variant);

@@ -360,15 +360,13 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
   int store = force_store >= 0 ? force_store : choose_store(layout, k, d_out);
-  const int tile_x = store == boysfn_dev::kStoreSoABlockTma ? boysfn_dev::kSoATmaTileX : boysfn_dev::kBlockX;
   if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) &&
-      !make_soa_tmap(&tmap, d_out, n, ld, R, tile_x))
+      !make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::block_tma_tile_x(store)))
     store = boysfn_dev::kStoreSoABlock;
-  if (store == boysfn_dev::kStoreAoSBlockTmaSwz && !make_aos_swz_tmap(&tmap, d_out, n, R, boysfn_dev::kBlockX))
+  if (store == boysfn_dev::kStoreAoSBlockTmaSwz &&
+      !make_aos_swz_tmap(&tmap, d_out, n, R, boysfn_dev::block_tma_tile_x(store)))
     store = boysfn_dev::kStoreAoSXpose;
-  const int threads = store == boysfn_dev::kStoreSoABlockTma   ? boysfn_dev::kSoATmaTileX
-                      : store == boysfn_dev::kStoreAoSBlockTma ? boysfn_dev::kAoSTmaTileX
-                                                               : boysfn_dev::kThreadsPerBlock;
+  const int threads = boysfn_dev::block_tma_tile_x(store);  // kThreadsPerBlock for the other kinds
   switch (store) {
     case boysfn_dev::kStoreSoABlockTma:
       fn = boysfn_dev::kernel_soa_block_tma(k, v);
@@ -380,15 +378,15 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
       break;
     case boysfn_dev::kStoreSoABlockTmaBin:
       fn = boysfn_dev::kernel_soa_block_tma_bin(k, v);
-      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTmaBin>(R, boysfn_dev::kBlockX);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTmaBin>(R, threads);
       break;
     case boysfn_dev::kStoreAoSBlockTmaBin:
       fn = boysfn_dev::kernel_aos_block_tma_bin(k, v);
-      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaBin>(R, boysfn_dev::kBlockX);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaBin>(R, threads);
       break;
     case boysfn_dev::kStoreAoSBlockTmaSwz:
       fn = boysfn_dev::kernel_aos_block_tma_swz(k, v);
-      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaSwz>(R, boysfn_dev::kBlockX);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaSwz>(R, threads);
       break;
     case boysfn_dev::kStoreSoA:
       fn = boysfn_dev::kernel_soa(k, v);

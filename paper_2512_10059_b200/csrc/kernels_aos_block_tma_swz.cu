@@ -9,7 +9,7 @@ namespace {
 template <int K, int V>
 const void* entry() {
   using D = VariantDegrees<K, V>;
-  return reinterpret_cast<const void*>(&boys_eval_block_tma_kernel<K, D::NA, D::MA, D::NB, D::MB, kStoreAoSBlockTmaSwz>);
+  return reinterpret_cast<const void*>(&boys_eval_block_tma_kernel<K, D::NA, D::MA, D::NB, D::MB, kStoreAoSBlockTmaSwz, kSwzTmaTileX>);
 }
 
 template <int K>

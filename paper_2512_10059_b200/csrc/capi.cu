@@ -309,16 +309,47 @@ int choose_store(int layout, int k, const double* d_out) {
   return (k == 6 || k == 8) ? boysfn_dev::kStoreAoSBlockTmaBin : boysfn_dev::kStoreAoSBlockTma;
 }
 
-// BOYSFN_GENERIC=1 routes every order through the generic kernel (tests).
-bool generic_forced() {
+// BOYSFN_GENERIC=1 routes every order through the run-time-k kernels, =2
+// through the per-warp one only (tests).
+int generic_forced() {
   const char* e = std::getenv("BOYSFN_GENERIC");
-  return e != nullptr && e[0] == '1';
+  return e != nullptr && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
 }
 
-// The run-time-k kernel: orders above 32 and forced regions above 32.
+// The run-time-k kernels: orders above 32 and forced regions above 32.  Block
+// tiles stored by the TMA engine where a tensor map / bulk copy applies,
+// otherwise (unaligned or strided output, a forced region, host-mapped
+// output) the per-warp kernel.
 int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out, int layout,
                    size_t ld, cudaStream_t stream, unsigned long long* d_bad, int force_region,
-                   unsigned long long* d_ctr = nullptr) {
+                   unsigned long long* d_ctr = nullptr, bool allow_tma = true) {
+  const int R = k + 1;
+  EvalParams p = t->params[k];
+  int na = t->deg_na[k], ma = t->deg_ma[k], nb = t->deg_nb, mb = t->deg_mb;
+  if (allow_tma && force_region < 0 && generic_forced() != 2) {
+    const bool soa = layout == BOYSFN_LAYOUT_SOA;
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof tmap);
+    const bool ok = soa ? make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::kBlockX)
+                        : (reinterpret_cast<uintptr_t>(d_out) & 15) == 0;
+    if (ok) {
+      const void* fn = boysfn_dev::kernel_generic_tma(soa);
+      const size_t smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTmaBin>(R, boysfn_dev::kBlockX);
+      int sms = 0, bps = 0;
+      if (int st = occupancy(fn, boysfn_dev::kBlockX, smem, &sms, &bps)) return st;
+      const size_t ntiles = (n + boysfn_dev::kBlockX - 1) / boysfn_dev::kBlockX;
+      const unsigned grid = static_cast<unsigned>(std::min<size_t>(ntiles, static_cast<size_t>(sms) * bps));
+      unsigned long long* counter = nullptr;
+      bool release = false;
+      if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
+      void* args[] = {&p, &na, &ma, &nb, &mb, &k, &d_x, &n, &d_out, &d_bad, &counter, &tmap};
+      const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kBlockX), args, smem, stream);
+      if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
+      if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
+      boysfn_internal::count_launch();
+      return BOYSFN_OK;
+    }
+  }
   const void* fn = boysfn_dev::kernel_generic();
   const int aos_flag = layout == BOYSFN_LAYOUT_AOS ? 1 : 0;
   const size_t smem = aos_flag ? sizeof(double) * boysfn_dev::kThreadsPerBlock *
@@ -328,8 +359,6 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
   if (int st = occupancy(fn, boysfn_dev::kThreadsPerBlock, smem, &sms, &bps)) return st;
   const size_t want = ((n + 31) / 32 + boysfn_dev::kWarpsPerBlock - 1) / boysfn_dev::kWarpsPerBlock;
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
-  EvalParams p = t->params[k];
-  int na = t->deg_na[k], ma = t->deg_ma[k], nb = t->deg_nb, mb = t->deg_mb;
   int aos = aos_flag;
   unsigned long long* counter = nullptr;
   bool release = false;
@@ -352,7 +381,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   if (!t->degree_ok[k])
     return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
   if (k > boysfn_dev::kKernelKmax || generic_forced())
-    return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1, d_ctr);
+    return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1, d_ctr, force_store < 0);
   const int R = k + 1;
   const int v = t->variant[k];
   const void* fn = nullptr;

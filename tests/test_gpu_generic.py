@@ -1,5 +1,7 @@
-"""The run-time-k generic kernel (boys_eval_generic_kernel): bit-identical to the
-templated kernels for every k <= 32 (BOYSFN_GENERIC=1 routes all orders to it),
+"""The run-time-k kernels (boys_eval_generic_tma_kernel, and the per-warp
+boys_eval_generic_kernel where no tensor map applies): bit-identical to the
+templated kernels for every k <= 32 (BOYSFN_GENERIC=1 routes all orders to the
+run-time-k kernels, =2 to the per-warp one),
 and the evaluator for table sets with k_max > 32 -- the reference's gen path
 allows k_max <= 64 -- checked against the C restatement of
 eval.cpp, which takes any k."""
@@ -30,10 +32,37 @@ def test_generic_bit_identical_to_templated(cuda, port, monkeypatch):
     for k in range(33):
         for layout in ("soa", "aos"):
             a = dev(cuda, xs, k, layout)
-            monkeypatch.setenv("BOYSFN_GENERIC", "1")
-            b = dev(cuda, xs, k, layout)
-            monkeypatch.delenv("BOYSFN_GENERIC")
-            assert np.array_equal(bits(a), bits(b)), (k, layout)
+            for mode in ("1", "2"):  # block-TMA run-time-k kernel, per-warp kernel
+                monkeypatch.setenv("BOYSFN_GENERIC", mode)
+                b = dev(cuda, xs, k, layout)
+                monkeypatch.delenv("BOYSFN_GENERIC")
+                assert np.array_equal(bits(a), bits(b)), (k, layout, mode)
+
+
+def test_generic_block_tma_equals_per_warp_above_32(cuda, port, monkeypatch):
+    """Orders above 32: the block-TMA kernel (region-sorted tiles, F staged as
+    produced) and the per-warp kernel agree bit for bit on ragged sizes, and
+    the first bad x is reported identically."""
+    t = table_k64()
+    for n in (1, 127, 128, 129, 20011):
+        xs = port.gen_uniform(n, 40 + n % 7, 0.0, 60.0)
+        for k in (33, 47, 64):
+            for layout in ("soa", "aos"):
+                a = dev(cuda, xs, k, layout, tables=t)
+                monkeypatch.setenv("BOYSFN_GENERIC", "2")
+                b = dev(cuda, xs, k, layout, tables=t)
+                monkeypatch.delenv("BOYSFN_GENERIC")
+                assert np.array_equal(bits(a), bits(b)), (n, k, layout)
+    xs = port.gen_uniform(5000, 3, 0.0, 60.0)
+    xs[[4001, 777]] = (np.nan, -2.0)
+    for mode in (None, "2"):
+        if mode:
+            monkeypatch.setenv("BOYSFN_GENERIC", mode)
+        o = np.full(xs.size * 41, 1.5)
+        with pytest.raises(pkg.domain_error) as ei:
+            pkg.boys_batch_many(xs, 40, t, o)
+        monkeypatch.delenv("BOYSFN_GENERIC", raising=False)
+        assert ei.value.first_bad == 777
 
 
 def table_k64():

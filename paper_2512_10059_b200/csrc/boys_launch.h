@@ -58,7 +58,8 @@ const void* kernel_aos_block_tma_bin(int k, int variant);
 const void* kernel_aos_block_tma_swz(int k, int variant);  // k = 15, 31 only
 const void* kernel_region(int k, int variant);
 const void* kernel_generic();
-const void* kernel_generic_tma(bool soa);
+const void* kernel_generic_tma(int k, bool soa);  // nullptr above 64
+const void* kernel_generic_stage(bool soa);
 
 // Exact degrees of the embedded kernels (from embedded_tables.inc).
 void embedded_degrees(int k, int* na, int* ma, int* nb, int* mb);

@@ -309,12 +309,17 @@ int choose_store(int layout, int k, const double* d_out) {
   return (k == 6 || k == 8) ? boysfn_dev::kStoreAoSBlockTmaBin : boysfn_dev::kStoreAoSBlockTma;
 }
 
-// BOYSFN_GENERIC=1 routes every order through the run-time-k kernels, =2
-// through the per-warp one only (tests).
+// BOYSFN_GENERIC=1 routes every order through the run-time-k kernels (by the
+// policy below), =2 through the per-warp one, =3 the staged block kernel, =4
+// the register-buffered block kernel (tests and experiments).
 int generic_forced() {
   const char* e = std::getenv("BOYSFN_GENERIC");
-  return e != nullptr && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
+  return e != nullptr && e[0] >= '1' && e[0] <= '4' ? e[0] - '0' : 0;
 }
+// Up to this order the staged block kernel (F written into the stage as it is
+// produced, 40 registers) beats the register-buffered one (F in registers
+// while the previous tile drains, 124-165 registers); profiles/r01_generic_kernel.txt.
+constexpr int kGenericStageKmax = 34;
 
 // The run-time-k kernels: orders above 32 and forced regions above 32.  Block
 // tiles stored by the TMA engine where a tensor map / bulk copy applies,
@@ -326,24 +331,28 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
   const int R = k + 1;
   EvalParams p = t->params[k];
   int na = t->deg_na[k], ma = t->deg_ma[k], nb = t->deg_nb, mb = t->deg_mb;
-  if (allow_tma && force_region < 0 && generic_forced() != 2) {
+  const int mode = generic_forced();
+  if (allow_tma && force_region < 0 && mode != 2) {
     const bool soa = layout == BOYSFN_LAYOUT_SOA;
     CUtensorMap tmap;
     std::memset(&tmap, 0, sizeof tmap);
-    const bool ok = soa ? make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::kBlockX)
+    const bool ok = soa ? make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::kGenericTileX)
                         : (reinterpret_cast<uintptr_t>(d_out) & 15) == 0;
-    if (ok) {
-      const void* fn = boysfn_dev::kernel_generic_tma(soa);
-      const size_t smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTmaBin>(R, boysfn_dev::kBlockX);
+    const bool staged = mode == 3 || (mode != 4 && k <= kGenericStageKmax);
+    const void* fn = staged ? boysfn_dev::kernel_generic_stage(soa) : boysfn_dev::kernel_generic_tma(k, soa);
+    if (ok && fn != nullptr) {
+      const int pitch = staged ? R : boysfn_dev::generic_stage_pitch(soa, R);
+      const size_t smem =
+          boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTmaBin>(pitch, boysfn_dev::kGenericTileX);
       int sms = 0, bps = 0;
-      if (int st = occupancy(fn, boysfn_dev::kBlockX, smem, &sms, &bps)) return st;
-      const size_t ntiles = (n + boysfn_dev::kBlockX - 1) / boysfn_dev::kBlockX;
+      if (int st = occupancy(fn, boysfn_dev::kGenericTileX, smem, &sms, &bps)) return st;
+      const size_t ntiles = (n + boysfn_dev::kGenericTileX - 1) / boysfn_dev::kGenericTileX;
       const unsigned grid = static_cast<unsigned>(std::min<size_t>(ntiles, static_cast<size_t>(sms) * bps));
       unsigned long long* counter = nullptr;
       bool release = false;
       if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
       void* args[] = {&p, &na, &ma, &nb, &mb, &k, &d_x, &n, &d_out, &d_bad, &counter, &tmap};
-      const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kBlockX), args, smem, stream);
+      const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kGenericTileX), args, smem, stream);
       if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
       if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
       boysfn_internal::count_launch();

@@ -7,9 +7,24 @@
 namespace boysfn_dev {
 
 const void* kernel_generic() { return reinterpret_cast<const void*>(&boys_eval_generic_kernel<>); }
-const void* kernel_generic_tma(bool soa) {
-  return soa ? reinterpret_cast<const void*>(&boys_eval_generic_tma_kernel<true>)
-             : reinterpret_cast<const void*>(&boys_eval_generic_tma_kernel<false>);
+const void* kernel_generic_stage(bool soa) {
+  return soa ? reinterpret_cast<const void*>(&boys_eval_generic_stage_kernel<true>)
+             : reinterpret_cast<const void*>(&boys_eval_generic_stage_kernel<false>);
+}
+// k <= 32, 36, 40, 48, 56, 64: the register array's bound
+const void* kernel_generic_tma(int k, bool soa) {
+#define BOYSFN_GT(KM)                                                                 \
+  if (k <= KM)                                                                        \
+    return soa ? reinterpret_cast<const void*>(&boys_eval_generic_tma_kernel<KM, true>) \
+               : reinterpret_cast<const void*>(&boys_eval_generic_tma_kernel<KM, false>);
+  BOYSFN_GT(32)
+  BOYSFN_GT(36)
+  BOYSFN_GT(40)
+  BOYSFN_GT(48)
+  BOYSFN_GT(56)
+  BOYSFN_GT(64)
+#undef BOYSFN_GT
+  return nullptr;
 }
 
 }  // namespace boysfn_dev

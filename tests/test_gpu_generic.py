@@ -1,7 +1,8 @@
 """The run-time-k kernels (boys_eval_generic_tma_kernel, and the per-warp
 boys_eval_generic_kernel where no tensor map applies): bit-identical to the
 templated kernels for every k <= 32 (BOYSFN_GENERIC=1 routes all orders to the
-run-time-k kernels, =2 to the per-warp one),
+run-time-k kernels, =2 to the per-warp one, =3 to the staged block kernel, =4 to
+the register-buffered block kernel),
 and the evaluator for table sets with k_max > 32 -- the reference's gen path
 allows k_max <= 64 -- checked against the C restatement of
 eval.cpp, which takes any k."""
@@ -32,7 +33,7 @@ def test_generic_bit_identical_to_templated(cuda, port, monkeypatch):
     for k in range(33):
         for layout in ("soa", "aos"):
             a = dev(cuda, xs, k, layout)
-            for mode in ("1", "2"):  # block-TMA run-time-k kernel, per-warp kernel
+            for mode in ("1", "2", "3", "4"):
                 monkeypatch.setenv("BOYSFN_GENERIC", mode)
                 b = dev(cuda, xs, k, layout)
                 monkeypatch.delenv("BOYSFN_GENERIC")
@@ -40,22 +41,24 @@ def test_generic_bit_identical_to_templated(cuda, port, monkeypatch):
 
 
 def test_generic_block_tma_equals_per_warp_above_32(cuda, port, monkeypatch):
-    """Orders above 32: the block-TMA kernel (region-sorted tiles, F staged as
-    produced) and the per-warp kernel agree bit for bit on ragged sizes, and
-    the first bad x is reported identically."""
+    """Orders above 32: the block-TMA kernels (region-sorted tiles; F staged as
+    produced, or held in registers while the previous tile drains) and the
+    per-warp kernel agree bit for bit on ragged sizes, and the first bad x is
+    reported identically."""
     t = table_k64()
     for n in (1, 127, 128, 129, 20011):
         xs = port.gen_uniform(n, 40 + n % 7, 0.0, 60.0)
-        for k in (33, 47, 64):
+        for k in (33, 35, 40, 47, 63, 64):  # even k+1: the padded AoS stage
             for layout in ("soa", "aos"):
                 a = dev(cuda, xs, k, layout, tables=t)
-                monkeypatch.setenv("BOYSFN_GENERIC", "2")
-                b = dev(cuda, xs, k, layout, tables=t)
-                monkeypatch.delenv("BOYSFN_GENERIC")
-                assert np.array_equal(bits(a), bits(b)), (n, k, layout)
+                for mode in ("2", "3", "4"):
+                    monkeypatch.setenv("BOYSFN_GENERIC", mode)
+                    b = dev(cuda, xs, k, layout, tables=t)
+                    monkeypatch.delenv("BOYSFN_GENERIC")
+                    assert np.array_equal(bits(a), bits(b)), (n, k, layout, mode)
     xs = port.gen_uniform(5000, 3, 0.0, 60.0)
     xs[[4001, 777]] = (np.nan, -2.0)
-    for mode in (None, "2"):
+    for mode in (None, "2", "3", "4"):
         if mode:
             monkeypatch.setenv("BOYSFN_GENERIC", mode)
         o = np.full(xs.size * 41, 1.5)

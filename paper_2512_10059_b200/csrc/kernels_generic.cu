@@ -7,9 +7,10 @@
 namespace boysfn_dev {
 
 const void* kernel_generic() { return reinterpret_cast<const void*>(&boys_eval_generic_kernel<>); }
+// the staged form (KM = 0)
 const void* kernel_generic_stage(bool soa) {
-  return soa ? reinterpret_cast<const void*>(&boys_eval_generic_stage_kernel<true>)
-             : reinterpret_cast<const void*>(&boys_eval_generic_stage_kernel<false>);
+  return soa ? reinterpret_cast<const void*>(&boys_eval_generic_tma_kernel<0, true>)
+             : reinterpret_cast<const void*>(&boys_eval_generic_tma_kernel<0, false>);
 }
 // k <= 32, 36, 40, 48, 56, 64: the register array's bound
 const void* kernel_generic_tma(int k, bool soa) {

@@ -439,11 +439,11 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
       break;
     case boysfn_dev::kStoreSoABinned:
       fn = boysfn_dev::kernel_soa_binned(k, v);
-      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * (R * boysfn_dev::kBinX + boysfn_dev::kBinX * 3 / 2);
+      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::binned_smem_doubles_per_warp(k, true);
       break;
     default:
       fn = boysfn_dev::kernel_aos_binned(k, v);
-      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * (R * boysfn_dev::kBinX + boysfn_dev::kBinX * 3 / 2);
+      smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::binned_smem_doubles_per_warp(k, false);
       break;
   }
   int sms = 0, bps = 0;

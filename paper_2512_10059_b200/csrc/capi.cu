@@ -266,6 +266,23 @@ bool make_aos_swz_tmap(CUtensorMap* m, double* out, size_t n, int R, int rows) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2D map over the AoS output for the run-time-k kernel's padded stage: dim0 =
+// order (R, contiguous), dim1 = row (stride 8R B); box = pitch x rows, so the
+// stage's pad columns (>= R) are outside the map and clipped by the store.
+bool make_aos_pad_tmap(CUtensorMap* m, double* out, size_t n, int R, int pitch, int rows) {
+  EncodeTiledFn enc = encode_tiled();
+  if (enc == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) || (R * sizeof(double)) % 16 ||
+      (pitch * sizeof(double)) % 16 || pitch > 256 || n > (size_t(1) << 31) - 256)
+    return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(R), n};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(R) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(pitch), static_cast<cuuint32_t>(rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Output-path selection (short-train medians of
 // every path at every k on one B200, profiles/r01_path_sweep.txt).  Large k is
 // HBM-write-bound and wants long contiguous write bursts: block tiles of 128 x
@@ -342,6 +359,9 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
     const void* fn = staged ? boysfn_dev::kernel_generic_stage(soa) : boysfn_dev::kernel_generic_tma(k, soa);
     if (ok && fn != nullptr) {
       const int pitch = staged ? R : boysfn_dev::generic_stage_pitch(soa, R);
+      int pad_tmap = 0;
+      if (!soa && pitch != R && std::getenv("BOYSFN_GENERIC_AOS_ROWS") == nullptr)
+        pad_tmap = make_aos_pad_tmap(&tmap, d_out, n, R, pitch, boysfn_dev::kGenericTileX) ? 1 : 0;
       const size_t smem =
           boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTmaBin>(pitch, boysfn_dev::kGenericTileX);
       int sms = 0, bps = 0;
@@ -351,7 +371,7 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
       unsigned long long* counter = nullptr;
       bool release = false;
       if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
-      void* args[] = {&p, &na, &ma, &nb, &mb, &k, &d_x, &n, &d_out, &d_bad, &counter, &tmap};
+      void* args[] = {&p, &na, &ma, &nb, &mb, &k, &d_x, &n, &d_out, &d_bad, &counter, &tmap, &pad_tmap};
       const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kGenericTileX), args, smem, stream);
       if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
       if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");

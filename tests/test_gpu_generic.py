@@ -19,11 +19,15 @@ pytestmark = pytest.mark.gpu
 
 
 def dev(torch, xs, k, layout, tables=None):
+    """F on the device; the 4 KB past the output must stay untouched (the
+    tensor stores clip rows >= n and the AoS stage's pad columns)."""
     x = torch.from_numpy(np.ascontiguousarray(xs)).cuda()
     n = xs.size
-    out = torch.empty(n * (k + 1), dtype=torch.float64, device="cuda")
+    buf = torch.full((n * (k + 1) + 512,), 7.25, dtype=torch.float64, device="cuda")
+    out = buf[: n * (k + 1)]
     pkg.eval_device(x, k, out, tables=tables, layout=layout)
     torch.cuda.synchronize()
+    assert bool((buf[n * (k + 1):] == 7.25).all()), "write past the output"
     o = out.cpu().numpy()
     return o.reshape(k + 1, n).T.copy() if layout == "soa" else o.reshape(n, k + 1)
 
@@ -51,10 +55,15 @@ def test_generic_block_tma_equals_per_warp_above_32(cuda, port, monkeypatch):
         for k in (33, 35, 40, 47, 63, 64):  # even k+1: the padded AoS stage
             for layout in ("soa", "aos"):
                 a = dev(cuda, xs, k, layout, tables=t)
-                for mode in ("2", "3", "4"):
-                    monkeypatch.setenv("BOYSFN_GENERIC", mode)
+                # "4r": the padded AoS stage's per-row bulk copies instead of
+                # its one clipped tensor store (BOYSFN_GENERIC_AOS_ROWS)
+                for mode in ("2", "3", "4", "4r"):
+                    monkeypatch.setenv("BOYSFN_GENERIC", mode[0])
+                    if mode == "4r":
+                        monkeypatch.setenv("BOYSFN_GENERIC_AOS_ROWS", "1")
                     b = dev(cuda, xs, k, layout, tables=t)
                     monkeypatch.delenv("BOYSFN_GENERIC")
+                    monkeypatch.delenv("BOYSFN_GENERIC_AOS_ROWS", raising=False)
                     assert np.array_equal(bits(a), bits(b)), (n, k, layout, mode)
     xs = port.gen_uniform(5000, 3, 0.0, 60.0)
     xs[[4001, 777]] = (np.nan, -2.0)

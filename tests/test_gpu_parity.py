@@ -331,3 +331,26 @@ def test_cuda_graph_capture_and_replay(cuda, port):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int64), eager.view(torch.int64))
+
+
+def test_binned_region_c_pairs_with_huge_x(cuda, port, monkeypatch):
+    """The binned kernels evaluate all-region-C virtual tiles two at a time
+    with the fast sqrt/division paths run unconditionally and the IEEE
+    operations re-run for lanes outside the fast range (boys_device.cuh:
+    boys_values_c_pair).  Groups made only of region-C x, with x >= 2^1022
+    scattered through them (including pairs where only one tile has such an x),
+    are bit-identical to the reference at every order the binned kernels run."""
+    rng = np.random.default_rng(11)
+    n = 4096 + 77  # whole 128- and 256-x groups plus a ragged tail
+    xs = rng.uniform(port.x1, 5e3, n)
+    huge = [2.0 ** 1022, np.nextafter(2.0 ** 1022, 0.0), 1e308, 1.7976931348623157e308]
+    for i, pos in enumerate((5, 70, 300, 301, 1000, 2050, 4100)):
+        xs[pos] = huge[i % len(huge)]
+    for k in range(7):
+        want = port.boys_batch_many(xs, k)
+        for layout in ("soa", "aos"):
+            monkeypatch.setenv("BOYSFN_SOA_PATH" if layout == "soa" else "BOYSFN_AOS_PATH", "binned")
+            got = device_eval(cuda, xs, k, layout)
+            monkeypatch.delenv("BOYSFN_SOA_PATH", raising=False)
+            monkeypatch.delenv("BOYSFN_AOS_PATH", raising=False)
+            assert np.array_equal(bits(got), bits(want)), (k, layout)

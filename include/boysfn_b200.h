@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define BOYSFN_ABI_VERSION 1
+#define BOYSFN_ABI_VERSION 2  /* 2: boysfn_eval_device takes out_len */
 
 /* Error convention.  The reference throws C++ exceptions; each maps to one code
  * and the C++ shim rethrows the same type with the same message. */
@@ -74,6 +74,10 @@ typedef struct boysfn_tables_s* boysfn_tables_t;
  * -- table sets with k_max > 32, e.g. from the reference's gen path
  * (k_max <= 64) -- run on the run-time-k generic kernel. */
 #define BOYSFN_DEVICE_KMAX 32
+/* Largest order any kernel evaluates (the run-time-k kernels; SPEC.md:476
+ * caps generated sets at k_max <= 64).  Sets with a larger k_max load, but
+ * orders above this return BOYSFN_ERR_UNSUPPORTED. */
+#define BOYSFN_DEVICE_KMAX_RT 64
 /* Largest numerator / denominator degree the device image holds. */
 #define BOYSFN_DEVICE_MAX_DEGREE 23
 
@@ -83,10 +87,17 @@ const char* boysfn_status_string(int status);
  * SIZE/DOMAIN/RANGE/TABLES, CUDA error text for CUDA). */
 const char* boysfn_last_error(void);
 
-/* Build a table handle from a table set; validates like validate_tables
- * (tables.cpp:14-32) and copies the coefficients.  Replaces passing
- * `const CoefficientTableSet&` (eval.hpp:44) across the boundary. */
+/* Build a table handle from a table set and copy the coefficients.  Replaces
+ * passing `const CoefficientTableSet&` (eval.hpp:44) across the boundary.
+ * Like eval.cpp, which evaluates any set it is given, it refuses only what
+ * the device image cannot hold: k_max < 0, a missing r_A array, empty or
+ * non-finite coefficient vectors (BOYSFN_ERR_TABLES, validate_tables'
+ * messages).  The full validate_tables outcome is recorded in the handle and
+ * enforced by boysfn_verify_tables, as verify.cpp:14 does. */
 int boysfn_tables_create(const boysfn_table_desc* desc, boysfn_tables_t* out);
+/* validate_tables (tables.cpp:14-32): same checks, order and messages;
+ * BOYSFN_ERR_TABLES with boysfn_last_error() set on the first failure. */
+int boysfn_tables_validate(const boysfn_table_desc* desc);
 /* Process-lifetime handle of the embedded Appendix-C set (k_max = 32,
  * eps = 5e-14), the device image of embedded_default() (tables_data.cpp:8). */
 int boysfn_tables_embedded(boysfn_tables_t* out);
@@ -97,15 +108,18 @@ int boysfn_tables_info(boysfn_tables_t tables, double* x0, double* x1, int* k_ma
 
 /* Device entry point: x and out already resident in HBM.  Evaluates
  * F_0..F_k for all n arguments, enqueued on `stream`, asynchronous.
- *   layout AOS: out[i*(k+1)+l]  (ld ignored)
- *   layout SOA: out[l*ld+i]     (ld >= n)
+ *   layout AOS: out[i*(k+1)+l]  (ld ignored)   needs out_len >= n*(k+1)
+ *   layout SOA: out[l*ld+i]     (ld >= n)      needs out_len >= k*ld + n
+ * out_len = doubles the caller owns at d_out; a smaller value returns
+ * BOYSFN_ERR_SIZE (the reference's size check, eval.cpp:90-91) and launches
+ * nothing.  Any alignment and any ld are accepted (TMA stores either way).
  * Invalid x (negative, NaN, +-inf) does not stop the launch: when
  * d_first_bad is non-NULL the kernel lowers *d_first_bad (a device uint64 the
  * caller initialised, e.g. to UINT64_MAX) to the smallest offending index with
  * atomicMin; rows at and after that index are unspecified.  Returns
  * BOYSFN_ERR_RANGE for k outside [0, k_max] (host-side, nothing launched). */
 int boysfn_eval_device(boysfn_tables_t tables, const double* d_x, size_t n, int k,
-                       double* d_out, int layout, size_t ld, void* stream,
+                       double* d_out, size_t out_len, int layout, size_t ld, void* stream,
                        unsigned long long* d_first_bad);
 
 /* Host entry point with boys_batch_many semantics (eval.cpp:88-96): xs and out

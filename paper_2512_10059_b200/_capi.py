@@ -43,13 +43,14 @@ _SIGNATURES = [
     ("boysfn_last_error", ctypes.c_char_p, []),
     ("boysfn_tables_create", ctypes.c_int, [ctypes.POINTER(TableDesc), ctypes.POINTER(ctypes.c_void_p)]),
     ("boysfn_tables_embedded", ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p)]),
+    ("boysfn_tables_validate", ctypes.c_int, [ctypes.POINTER(TableDesc)]),
     ("boysfn_tables_destroy", ctypes.c_int, [ctypes.c_void_p]),
     ("boysfn_tables_info", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int),
                                           ctypes.POINTER(ctypes.c_double)]),
     ("boysfn_eval_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
-                                          ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
-                                          ctypes.c_void_p]),
+                                          ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t,
+                                          ctypes.c_void_p, ctypes.c_void_p]),
     ("boysfn_eval_host", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
                                         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t,
                                         ctypes.POINTER(ctypes.c_size_t)]),

@@ -42,7 +42,10 @@ class Handle {
       return boysfn_rational_desc{r.degree_n(), r.degree_m(), r.numer.data(), r.denom.data()};
     };
     for (size_t k = 0; k < t.r_A.size(); ++k) ra[k] = desc(t.r_A[k]);
-    validate_tables(t);  // exact reference messages, incl. the r_A count check
+    // eval.cpp evaluates any set it is given: only what the device image needs
+    // is checked here (boysfn_tables_create); verify_tables validates first.
+    if (t.k_max >= 0 && t.r_A.size() < static_cast<size_t>(t.k_max) + 1)
+      throw std::invalid_argument("tables: need exactly k_max+1 region-A tables");
     const boysfn_table_desc d{t.x0, t.x1, t.k_max, t.eps_tol, desc(t.r_B), ra.data()};
     raise(boysfn_tables_create(&d, &h_));
   }
@@ -100,6 +103,7 @@ BoysBatch boys_batch_region(double x, int k, const CoefficientTableSet& tables, 
 
 VerifyReport verify_tables(const CoefficientTableSet& tables, int samples_per_region, double xmax,
                            std::uint64_t seed) {
+  validate_tables(tables);  // verify.cpp:14
   const Handle h(tables);
   std::vector<double> per_k((static_cast<size_t>(tables.k_max) + 1) * 3);
   boysfn_verify_report r{};

@@ -96,6 +96,29 @@ int validate_desc(const boysfn_table_desc* d) {
   return BOYSFN_OK;
 }
 
+// What the device image needs to evaluate a set (eval.cpp itself never
+// validates): k_max >= 0, k_max + 1 region-A tables, non-empty finite
+// coefficient vectors.  Messages as validate_tables' for the same faults.
+// Degrees above 23 are accepted here and refused per order at launch.
+int check_device_desc(const boysfn_table_desc* d) {
+  if (d->k_max < 0) return fail(BOYSFN_ERR_TABLES, "tables: k_max must be non-negative");
+  if (d->r_A == nullptr)
+    return fail(BOYSFN_ERR_TABLES, "tables: need exactly k_max+1 region-A tables");
+  auto check = [](const boysfn_rational_desc& r, const std::string& what) -> int {
+    if (r.n < 0 || r.m < 0 || r.numer == nullptr || r.denom == nullptr)
+      return fail(BOYSFN_ERR_TABLES, "tables: empty coefficient vector in " + what);
+    for (int i = 0; i <= r.n; ++i)
+      if (!std::isfinite(r.numer[i])) return fail(BOYSFN_ERR_TABLES, "tables: non-finite value in " + what);
+    for (int i = 0; i <= r.m; ++i)
+      if (!std::isfinite(r.denom[i])) return fail(BOYSFN_ERR_TABLES, "tables: non-finite value in " + what);
+    return BOYSFN_OK;
+  };
+  if (int st = check(d->r_B, "r_B")) return st;
+  for (int k = 0; k <= d->k_max; ++k)
+    if (int st = check(d->r_A[k], "r_A[" + std::to_string(k) + "]")) return st;
+  return BOYSFN_OK;
+}
+
 int build_handle(const boysfn_table_desc* d, boysfn_tables_s* h) {
   h->x0 = d->x0;
   h->x1 = d->x1;
@@ -409,6 +432,8 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   if (n == 0) return BOYSFN_OK;
   if (!t->degree_ok[k])
     return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
+  if (k > BOYSFN_DEVICE_KMAX_RT)
+    return fail(BOYSFN_ERR_UNSUPPORTED, "order above the run-time-k kernels' bound (64)");
   if (k > boysfn_dev::kKernelKmax || generic_forced())
     return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1, d_ctr, force_store < 0);
   const int R = k + 1;
@@ -487,9 +512,12 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
 }
 
 // --------------------------------------------------------- host pipeline --
-// Per (thread, device) staging: three slots, each with its own stream; a
-// chunk's H2D copy, kernel and D2H copy follow one another on its slot's
-// stream, and the slots overlap, so the link stays busy.
+// Staging for one host call on one device: three slots, each with its own
+// stream; a chunk's H2D copy, kernel and D2H copy follow one another on its
+// slot's stream, and the slots overlap, so the link stays busy.  Every buffer
+// is allocated on first use by the path that needs it (a small call never
+// touches the chunk buffers), and pipelines come from a bounded per-device
+// pool shared by all host threads (PipelinePool below).
 struct Pipeline {
   static constexpr int kSlots = 3;
   static constexpr size_t kChunkOutBytes = size_t(256) << 20;  // profiles/r01_e2e_chunk.txt
@@ -499,10 +527,12 @@ struct Pipeline {
   double* d_x[kSlots] = {};
   double* d_out[kSlots] = {};
   unsigned long long* d_ctr = nullptr;  // kSlots scheduler counters (slot s: only on stream[s])
-  size_t cap_x = 0;                     // x capacity per slot
-  size_t cap_out = 0;                   // doubles per slot
+  size_t cap_x = 0;                     // x capacity per slot (allocated)
+  size_t cap_out = 0;                   // output doubles per slot (the chunk size; allocated lazily)
+  bool have_out = false;
   double* h_x[kSlots] = {};             // pinned staging for pageable callers (lazy)
   double* h_out[kSlots] = {};
+  size_t cap_hx = 0;
   // small-batch path (lazy): host-mapped x and F the kernel reads and writes
   // over PCIe directly, so a small call is one launch and one sync
   static constexpr size_t kSmallValues = size_t(1) << 20;  // capacity, doubles
@@ -523,10 +553,24 @@ struct Pipeline {
     if (const char* e = std::getenv("BOYSFN_CHUNK_MB"))  // A/B experiments
       chunk = std::max<size_t>(1, std::strtoull(e, nullptr, 10)) << 20;
     cap_out = chunk / sizeof(double);
-    cap_x = cap_out;  // enough for k = 0
-    for (int s = 0; s < kSlots; ++s) {
-      CUDA_TRY(cudaMalloc(&d_x[s], cap_x * sizeof(double)));
-      CUDA_TRY(cudaMalloc(&d_out[s], cap_out * sizeof(double)));
+    return BOYSFN_OK;
+  }
+
+  // Device chunk buffers for chunks of cx x: the output slots once, the x
+  // slots sized to cx (grown if a later call needs more; every earlier call
+  // has synchronised its streams before returning).
+  int ensure_chunks(size_t cx) {
+    if (!have_out) {
+      for (int s = 0; s < kSlots; ++s) CUDA_TRY(cudaMalloc(&d_out[s], cap_out * sizeof(double)));
+      have_out = true;
+    }
+    if (cap_x < cx) {
+      for (int s = 0; s < kSlots; ++s) {
+        CUDA_TRY(cudaFree(d_x[s]));
+        d_x[s] = nullptr;
+        CUDA_TRY(cudaMalloc(&d_x[s], cx * sizeof(double)));
+      }
+      cap_x = cx;
     }
     return BOYSFN_OK;
   }
@@ -560,13 +604,101 @@ struct Pipeline {
     return BOYSFN_OK;
   }
 
-  int ensure_staging() {
-    for (int s = 0; s < kSlots; ++s) {
-      if (h_x[s] == nullptr) CUDA_TRY(cudaHostAlloc(&h_x[s], cap_x * sizeof(double), cudaHostAllocDefault));
-      if (h_out[s] == nullptr) CUDA_TRY(cudaHostAlloc(&h_out[s], cap_out * sizeof(double), cudaHostAllocDefault));
+  // Pinned host staging for pageable callers: x slots of cx, output slots of
+  // the chunk size.
+  int ensure_staging(size_t cx) {
+    if (cap_hx < cx) {
+      for (int s = 0; s < kSlots; ++s) {
+        CUDA_TRY(cudaFreeHost(h_x[s]));
+        h_x[s] = nullptr;
+        CUDA_TRY(cudaHostAlloc(&h_x[s], cx * sizeof(double), cudaHostAllocDefault));
+      }
+      cap_hx = cx;
     }
+    for (int s = 0; s < kSlots; ++s)
+      if (h_out[s] == nullptr) CUDA_TRY(cudaHostAlloc(&h_out[s], cap_out * sizeof(double), cudaHostAllocDefault));
     return BOYSFN_OK;
   }
+};
+
+// Pipelines per device, shared by every host thread: a call takes a free one
+// (creating it while fewer than the bound exist) and gives it back when it
+// returns, so N concurrent callers hold at most the bound's worth of device
+// and pinned memory (a drop-in boys_batch_many called from 64 OpenMP threads
+// would otherwise reserve 64 pipelines).  Further callers wait for a free
+// pipeline; they share one PCIe link anyway.  BOYSFN_MAX_PIPELINES overrides
+// the bound.  Never destroyed: at process exit the CUDA runtime may already
+// be gone.
+class PipelinePool {
+ public:
+  static PipelinePool& get() {
+    static PipelinePool* pool = new PipelinePool;
+    return *pool;
+  }
+  int acquire(int dev, Pipeline** out) {
+    std::unique_lock<std::mutex> lk(mu_);
+    auto& d = devs_[dev];
+    cv_.wait(lk, [&] { return !d.free.empty() || d.count < bound_; });
+    if (!d.free.empty()) {
+      *out = d.free.back();
+      d.free.pop_back();
+      return BOYSFN_OK;
+    }
+    ++d.count;  // reserve the slot, build outside the lock
+    lk.unlock();
+    auto* p = new Pipeline;
+    const int st = p->init(dev);
+    if (st != BOYSFN_OK) {
+      delete p;
+      lk.lock();
+      --d.count;
+      cv_.notify_one();
+      return st;
+    }
+    *out = p;
+    return BOYSFN_OK;
+  }
+  void release(Pipeline* p) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      devs_[p->device].free.push_back(p);
+    }
+    cv_.notify_one();
+  }
+  int bound() const { return bound_; }
+
+ private:
+  PipelinePool() {
+    if (const char* e = std::getenv("BOYSFN_MAX_PIPELINES")) bound_ = std::max(1, std::atoi(e));
+  }
+  struct PerDevice {
+    std::vector<Pipeline*> free;
+    int count = 0;
+  };
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::map<int, PerDevice> devs_;
+  int bound_ = 4;
+};
+
+// A pipeline of the calling thread's current device for the duration of one call.
+class PipelineLease {
+ public:
+  PipelineLease() = default;
+  PipelineLease(const PipelineLease&) = delete;
+  PipelineLease& operator=(const PipelineLease&) = delete;
+  ~PipelineLease() {
+    if (p_ != nullptr) PipelinePool::get().release(p_);
+  }
+  int acquire() {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    return PipelinePool::get().acquire(dev, &p_);
+  }
+  Pipeline* get() const { return p_; }
+
+ private:
+  Pipeline* p_ = nullptr;
 };
 
 // Page-locked (or registered) host memory can be DMA'd directly; pageable
@@ -692,20 +824,6 @@ void parallel_copy(std::vector<Segment> segs) {
   CopyPool::get().run(pieces, T);
 }
 
-int get_pipeline(Pipeline** out) {
-  thread_local std::map<int, std::unique_ptr<Pipeline>> pipes;
-  int dev = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  auto& p = pipes[dev];
-  if (!p) {
-    auto np = std::make_unique<Pipeline>();
-    if (int st = np->init(dev)) return st;
-    p = std::move(np);
-  }
-  *out = p.get();
-  return BOYSFN_OK;
-}
-
 bool x_ok(double x) { return std::isfinite(x) && x >= 0; }
 
 // NVTX range for timeline tools (Nsight Systems): the host API's phases.
@@ -774,11 +892,19 @@ BOYSFN_API const char* boysfn_last_error(void) { return t_last_error.c_str(); }
 
 BOYSFN_API int boysfn_tables_create(const boysfn_table_desc* desc, boysfn_tables_t* out) {
   if (desc == nullptr || out == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
-  if (int st = validate_desc(desc)) return st;
+  if (int st = check_device_desc(desc)) return st;
   auto* h = new boysfn_tables_s;
   build_handle(desc, h);
+  h->valid_status = validate_desc(desc);
+  if (h->valid_status != BOYSFN_OK) h->valid_msg = boysfn_last_error();
+  t_last_error.clear();
   *out = h;
   return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_tables_validate(const boysfn_table_desc* desc) {
+  if (desc == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
+  return validate_desc(desc);
 }
 
 BOYSFN_API int boysfn_tables_embedded(boysfn_tables_t* out) {
@@ -803,7 +929,7 @@ BOYSFN_API int boysfn_tables_info(boysfn_tables_t t, double* x0, double* x1, int
 }
 
 BOYSFN_API int boysfn_eval_device(boysfn_tables_t t, const double* d_x, size_t n, int k,
-                                  double* d_out, int layout, size_t ld, void* stream,
+                                  double* d_out, size_t out_len, int layout, size_t ld, void* stream,
                                   unsigned long long* d_first_bad) {
   if (t == nullptr) return fail(BOYSFN_ERR_ARG, "null handle");
   if (k < 0 || k > t->k_max) return fail(BOYSFN_ERR_RANGE, kMsgRange);
@@ -812,6 +938,8 @@ BOYSFN_API int boysfn_eval_device(boysfn_tables_t t, const double* d_x, size_t n
   if (n == 0) return BOYSFN_OK;
   if (d_x == nullptr || d_out == nullptr) return fail(BOYSFN_ERR_ARG, "null buffer");
   if (layout == BOYSFN_LAYOUT_SOA && ld < n) return fail(BOYSFN_ERR_ARG, "SOA ld must be >= n");
+  const size_t need = layout == BOYSFN_LAYOUT_AOS ? n * (static_cast<size_t>(k) + 1) : static_cast<size_t>(k) * ld + n;
+  if (out_len < need) return fail(BOYSFN_ERR_SIZE, kMsgSize);
   return launch_eval(t, d_x, n, k, d_out, layout, ld, static_cast<cudaStream_t>(stream),
                      d_first_bad);
 }
@@ -852,8 +980,9 @@ int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double*
   const NvtxRange range("boysfn_eval_host");
   const size_t row = static_cast<size_t>(k) + 1;
   const size_t out_len = out_extent;
-  Pipeline* P = nullptr;
-  if (int st = get_pipeline(&P)) return st;
+  PipelineLease lease;
+  if (int st = lease.acquire()) return st;
+  Pipeline* P = lease.get();
   if (const char* e = std::getenv("BOYSFN_SMALL_VALUES"))  // A/B experiments
     P->small_limit = std::min<size_t>(Pipeline::kSmallValues, std::strtoull(e, nullptr, 10));
   if (n * row <= P->small_limit && std::getenv("BOYSFN_NO_SMALL_PATH") == nullptr) {
@@ -882,13 +1011,16 @@ int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double*
     }
     return BOYSFN_OK;
   }
-  const size_t cx = std::max<size_t>(32, std::min(P->cap_x, P->cap_out / row) / 32 * 32);
+  // chunks of cx x (a multiple of 32): the output slot's worth of rows, at
+  // most n rounded up
+  const size_t cx = std::max<size_t>(32, std::min(P->cap_out / row, (n + 31) / 32 * 32) / 32 * 32);
   const size_t nchunks = (n + cx - 1) / cx;
   const int S = Pipeline::kSlots;
   const bool x_direct = is_pinned(xs) && is_pinned(xs + n - 1);
   const bool out_direct = is_pinned(out) && is_pinned(out + out_len - 1);
+  if (int st = P->ensure_chunks(cx)) return st;
   if (!(x_direct && out_direct))
-    if (int st = P->ensure_staging()) return st;
+    if (int st = P->ensure_staging(cx)) return st;
 
   // Chunk c in slot s = c % S, all on stream s: (stage x) -> H2D -> kernel ->
   // D2H of the rows before the first bad x -> event.  x is checked on the host
@@ -1127,24 +1259,28 @@ BOYSFN_API int boysfn_eval_region_host(boysfn_tables_t t, double x, int k, int r
   if (!x_ok(x)) return fail(BOYSFN_ERR_DOMAIN, kMsgDomain);
   if (k < 0 || k > t->k_max) return fail(BOYSFN_ERR_RANGE, kMsgRange);
   if (region == BOYSFN_REGION_B && !(x > 0)) return fail(BOYSFN_ERR_DOMAIN, kMsgUpward);
-  Pipeline* P = nullptr;
-  if (int st = get_pipeline(&P)) return st;
-  cudaStream_t s = P->stream[0];
-  CUDA_TRY(cudaStreamSynchronize(s));
   if (!t->degree_ok[k]) return fail(BOYSFN_ERR_UNSUPPORTED, "table degree exceeds the device image (max 23)");
+  if (k > BOYSFN_DEVICE_KMAX_RT)
+    return fail(BOYSFN_ERR_UNSUPPORTED, "order above the run-time-k kernels' bound (64)");
+  PipelineLease lease;
+  if (int st = lease.acquire()) return st;
+  Pipeline* P = lease.get();
+  // one x in, one row out, through the host-mapped small-call buffers
+  if (int st = P->ensure_small()) return st;
+  cudaStream_t s = P->stream[0];
+  P->hs_x[0] = x;
   if (k > boysfn_dev::kKernelKmax) {
-    CUDA_TRY(cudaMemcpyAsync(P->d_x[0], &x, sizeof(double), cudaMemcpyHostToDevice, s));
-    if (int st = launch_generic(t, P->d_x[0], 1, k, P->d_out[0], BOYSFN_LAYOUT_AOS, 1, s, nullptr, region,
-                                P->d_ctr))
+    if (int st = launch_generic(t, P->ds_x, 1, k, P->ds_out, BOYSFN_LAYOUT_AOS, 1, s, nullptr, region, P->d_ctr,
+                                false))
       return st;
   } else {
     EvalParams p = t->params[k];
-    void* args[] = {&p, &x, &region, &P->d_out[0]};
+    void* args[] = {&p, &x, &region, &P->ds_out};
     CUDA_TRY(cudaLaunchKernel(boysfn_dev::kernel_region(k, t->variant[k]), dim3(1), dim3(1), args, 0, s));
     boysfn_internal::count_launch();
   }
-  CUDA_TRY(cudaMemcpyAsync(out, P->d_out[0], (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  std::memcpy(out, P->hs_out, (k + 1) * sizeof(double));
   return BOYSFN_OK;
 }
 

@@ -21,6 +21,11 @@ struct boysfn_tables_s {
   std::vector<int> degree_ok;                  // 1 if r_A[k], r_B fit the device image
   std::vector<int> deg_na, deg_ma;             // degrees of r_A[k] (generic kernel)
   int deg_nb = 0, deg_mb = 0;                  // degrees of r_B
+  // validate_tables (tables.cpp:14-32) outcome, recorded at creation: the
+  // evaluation paths do not need it (eval.cpp never validates), verify_tables
+  // does (verify.cpp:14)
+  int valid_status = 0;
+  std::string valid_msg;
 };
 
 namespace boysfn_internal {

@@ -94,7 +94,8 @@ BOYSFN_API int boysfn_verify_tables(boysfn_tables_t t, int samples_per_region, d
                                     boysfn_verify_report* rep) {
   using boysfn_internal::fail;
   if (t == nullptr || rep == nullptr || rep->per_k == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
-  // verify.cpp:14-18
+  // verify.cpp:14-18 (validate_tables, recorded when the handle was built)
+  if (t->valid_status != BOYSFN_OK) return fail(t->valid_status, t->valid_msg);
   if (samples_per_region < 1)
     return fail(BOYSFN_ERR_INVALID, "verify_tables: need at least one sample per region");
   if (xmax <= t->x1) return fail(BOYSFN_ERR_INVALID, "verify_tables: xmax must exceed x1");
@@ -156,7 +157,7 @@ BOYSFN_API int boysfn_verify_tables(boysfn_tables_t t, int samples_per_region, d
     dd_oracle_kernel<<<grid, 128, 0, s>>>(d_x, d_terms, n, kmax, d_oracle);
     boysfn_internal::count_launch();
     for (int k = 0; k <= kmax && status == BOYSFN_OK; ++k) {
-      status = boysfn_eval_device(t, d_x, n, k, d_got, BOYSFN_LAYOUT_AOS, 0, s, nullptr);
+      status = boysfn_eval_device(t, d_x, n, k, d_got, n * (k + 1), BOYSFN_LAYOUT_AOS, 0, s, nullptr);
       if (status) break;
       compare_kernel<<<grid, 128, 0, s>>>(d_got, d_oracle, n, samples_per_region, k, kmax, d_max + 3 * k);
       boysfn_internal::count_launch();
@@ -190,7 +191,7 @@ BOYSFN_API int boysfn_verify_tables(boysfn_tables_t t, int samples_per_region, d
         bool has = false;
         for (int r = 0; r < 3; ++r) has |= rep->per_k[3 * k + r] == rep->max_err;
         if (!has) continue;
-        status = boysfn_eval_device(t, d_x, n, k, d_got, BOYSFN_LAYOUT_AOS, 0, s, nullptr);
+        status = boysfn_eval_device(t, d_x, n, k, d_got, n * (k + 1), BOYSFN_LAYOUT_AOS, 0, s, nullptr);
         if (status) break;
         cudaMemset(d_first, 0xFF, sizeof(unsigned long long));
         const unsigned grid = static_cast<unsigned>(std::min<size_t>((n + 127) / 128, 148 * 16));

@@ -86,7 +86,11 @@ class DeviceTables:
         if not self._owned:
             _raise(L.boysfn_tables_embedded(ctypes.byref(self._h)))
             return
-        validate_tables(tables)
+        # eval.cpp evaluates any set it is given; the device image needs only
+        # k_max+1 region-A tables with finite coefficients (checked by
+        # boysfn_tables_create).  Extra r_A entries are ignored.
+        if len(tables.r_A) < tables.k_max + 1:
+            raise invalid_argument("tables: need exactly k_max+1 region-A tables")
         keep = []
 
         def desc(r):
@@ -96,7 +100,7 @@ class DeviceTables:
             return _capi.RationalDesc(len(nu) - 1, len(de) - 1,
                                       nu.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                       de.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
-        ra = (_capi.RationalDesc * len(tables.r_A))(*[desc(r) for r in tables.r_A])
+        ra = (_capi.RationalDesc * (tables.k_max + 1))(*[desc(r) for r in tables.r_A[: tables.k_max + 1]])
         d = _capi.TableDesc(tables.x0, tables.x1, tables.k_max, tables.eps_tol, desc(tables.r_B), ra)
         _raise(L.boysfn_tables_create(ctypes.byref(d), ctypes.byref(self._h)))
 
@@ -182,12 +186,37 @@ def boys_batch_region(x, k, tables, region):
     return BoysBatch(float(x), int(k), out[: int(k) + 1].tolist())
 
 
+def _check_device_tensor(name, t, dtype, device=None):
+    """A tensor handed to the C ABI as a raw device pointer: right dtype,
+    contiguous, on a CUDA device (the same one as x)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise invalid_argument("%s must be a torch CUDA tensor" % name)
+    if t.dtype != dtype:
+        raise invalid_argument("%s must be %s, got %s" % (name, dtype, t.dtype))
+    if not t.is_cuda:
+        raise invalid_argument("%s must be on a CUDA device" % name)
+    if device is not None and t.device != device:
+        raise invalid_argument("%s is on %s, x on %s" % (name, t.device, device))
+    if not t.is_contiguous():
+        raise invalid_argument("%s must be contiguous" % name)
+
+
 def eval_device(x, k, out, tables=None, layout="soa", ld=None, stream=None, first_bad=None):
     """HBM-resident entry point: x a CUDA float64 tensor of N arguments, out a
-    CUDA float64 tensor ((k+1)*ld for SoA, N*(k+1) for AoS).  Enqueued on
-    `stream` (default: torch's current stream), asynchronous.  first_bad: an
-    optional CUDA int64 tensor lowered to the smallest invalid index."""
+    CUDA float64 tensor (at least k*ld+N doubles for SoA, N*(k+1) for AoS;
+    boysfn_eval_device checks the size).  Enqueued on `stream` (default:
+    torch's current stream), asynchronous.  first_bad: an optional CUDA int64
+    tensor lowered to the smallest invalid index."""
     import torch
+    if layout not in ("soa", "aos"):
+        raise invalid_argument("layout must be 'soa' or 'aos'")
+    _check_device_tensor("x", x, torch.float64)
+    _check_device_tensor("out", out, torch.float64, x.device)
+    if first_bad is not None:
+        _check_device_tensor("first_bad", first_bad, torch.int64, x.device)
+        if first_bad.numel() < 1:
+            raise invalid_argument("first_bad must hold one element")
     L = _capi.lib()
     tables = tables if tables is not None else embedded_default()
     h = _handle(tables)
@@ -195,7 +224,7 @@ def eval_device(x, k, out, tables=None, layout="soa", ld=None, stream=None, firs
     lay = _capi.LAYOUT_SOA if layout == "soa" else _capi.LAYOUT_AOS
     ld = n if ld is None else int(ld)
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
-    st = L.boysfn_eval_device(h.handle, x.data_ptr(), n, int(k), out.data_ptr(), lay, ld,
+    st = L.boysfn_eval_device(h.handle, x.data_ptr(), n, int(k), out.data_ptr(), out.numel(), lay, ld,
                               ctypes.c_void_p(s.cuda_stream),
                               first_bad.data_ptr() if first_bad is not None else None)
     _raise(st)
@@ -230,10 +259,19 @@ def alg2(x, y, c, k=None, z=None, tables=None, stream=None):
     the device.  x, y: CUDA float64 tensors of n; c: k+1 host floats; returns
     z (a new CUDA tensor unless given).  Asynchronous on `stream`."""
     import torch
-    c = np.ascontiguousarray(c, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64).ravel()
     k = len(c) - 1 if k is None else int(k)
+    if k < 0 or len(c) < k + 1:
+        raise invalid_argument("alg2: c needs k+1 = %d coefficients, got %d" % (k + 1, len(c)))
+    _check_device_tensor("x", x, torch.float64)
+    _check_device_tensor("y", y, torch.float64, x.device)
+    if y.numel() != x.numel():
+        raise invalid_argument("alg2: y must have as many elements as x")
     if z is None:
         z = torch.empty_like(x)
+    _check_device_tensor("z", z, torch.float64, x.device)
+    if z.numel() != x.numel():
+        raise invalid_argument("alg2: z must have as many elements as x")
     tables = tables if tables is not None else embedded_default()
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
     h = _handle(tables)  # keep the handle alive across the call
@@ -269,6 +307,7 @@ class VerifyReport:
 def verify_tables(tables, samples_per_region, xmax=200.0, seed=1):
     """verify_tables (verify.hpp:34-35) on the GPU: the reference's sampling,
     every order, a double-double oracle; same report fields."""
+    validate_tables(tables)  # verify.cpp:14
     per_k = (ctypes.c_double * ((tables.k_max + 1) * 3))()
     rep = _capi.VerifyReportC()
     rep.per_k = per_k

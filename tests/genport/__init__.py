@@ -2,7 +2,8 @@
 region partition, weighted rational Remez exchange, Walsh-table degree search
 and the gen pipeline, restated from the reference's regions/remez/polynomial/
 linalg/highprec/reference sources in mpmath, with the extremum scan on the
-B200 (scan.py).  Offline tooling: the evaluator never imports it."""
+B200 (scan.py).  Test-only cross-check of the native generator (cpp/src/gen): the evaluator
+never imports it."""
 from .hp import (boys_reference, boys_reference_batch, erf, erfc, gamma_half, precision,  # noqa: F401
                  reference_terms_for, set_working_digits, truncation_bound, upper_gamma_half, working_digits)
 from .linalg import jacobi_eigensolve  # noqa: F401

@@ -13,7 +13,7 @@ from typing import List, Optional
 
 from mpmath import mpf
 
-from .. import tables as T
+from paper_2512_10059_b200 import tables as T
 from . import hp
 from .regions import compute_x0, compute_x1, weight_rho_A
 from .remez import WalshResult, walsh_search
@@ -85,7 +85,7 @@ def certify(tables, alternatives, samples=10000, xmax=200.0, seed=1, log=None):
     error of the exact rational, which does not see the rounding of the
     coefficients to double or the double-precision recurrence).  Returns
     (passed, report)."""
-    from ..eval import verify_tables
+    from paper_2512_10059_b200.eval import verify_tables
     rep = verify_tables(tables, samples, xmax, seed)
     tried = {k: 0 for k in range(tables.k_max + 1)}
     while rep.max_err > tables.eps_tol:

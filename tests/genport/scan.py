@@ -19,7 +19,7 @@ import ctypes
 import numpy as np
 from mpmath import mpf
 
-from .. import _capi
+from paper_2512_10059_b200 import _capi
 from . import hp
 
 WEIGHTS = {"one": 0, "rho_A": 1}

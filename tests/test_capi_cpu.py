@@ -54,7 +54,7 @@ def test_no_cudart_symbols_leak():
 
 def test_abi_and_status_strings():
     lib = _capi.lib()
-    assert lib.boysfn_abi_version() == 1
+    assert lib.boysfn_abi_version() == 2
     for st in range(8):
         assert lib.boysfn_status_string(st)
 
@@ -69,7 +69,10 @@ def test_embedded_handle_info():
     assert (x0.value, x1.value, km.value, eps.value) == (s.x0, s.x1, s.k_max, s.eps_tol)
 
 
-def test_tables_create_validates_like_reference():
+def test_tables_create_checks_only_what_the_device_needs():
+    """eval.cpp never validates: a set it evaluates (non-monic denominator,
+    eps_tol 0, x0 >= x1) loads; non-finite or empty coefficients do not.
+    boysfn_tables_validate is validate_tables (tables.cpp:14-32)."""
     import copy
     lib = _capi.lib()
     h = pkg.DeviceTables(copy.deepcopy(pkg.embedded_default()))  # host-only: no device allocation
@@ -78,15 +81,45 @@ def test_tables_create_validates_like_reference():
     bad.r_B.numer[2] = float("inf")
     with pytest.raises(ValueError, match="tables: non-finite value in r_B"):
         pkg.DeviceTables(bad)
-    # the C ABI itself (bypassing the Python validation) gives the same message
+    odd = copy.deepcopy(pkg.embedded_default())
+    odd.eps_tol = 0.0
+    odd.r_A[3].denom[-1] = 2.0
+    pkg.DeviceTables(odd).close()
     nu = (ctypes.c_double * 1)(1.0)
     de = (ctypes.c_double * 1)(0.5)
     r = _capi.RationalDesc(0, 0, nu, de)
     ra = (_capi.RationalDesc * 1)(r)
     d = _capi.TableDesc(1.0, 2.0, 0, 1e-8, r, ra)
     out = ctypes.c_void_p()
-    assert lib.boysfn_tables_create(ctypes.byref(d), ctypes.byref(out)) == _capi.ERR_TABLES
+    assert lib.boysfn_tables_create(ctypes.byref(d), ctypes.byref(out)) == 0
+    lib.boysfn_tables_destroy(out)
+    # validate_tables itself, through the C ABI: the reference's message
+    assert lib.boysfn_tables_validate(ctypes.byref(d)) == _capi.ERR_TABLES
     assert _capi.last_error() == "tables: non-monic denominator in r_B"
+    # verify_tables validates first (verify.cpp:14), before any device work
+    with pytest.raises(ValueError, match="tables: eps_tol must be positive"):
+        pkg.verify_tables(odd, 10)
+
+
+def test_eval_device_size_check_needs_no_device():
+    """boysfn_eval_device refuses an output shorter than the layout needs
+    (AoS n(k+1), SoA k*ld+n) before touching the device."""
+    lib = _capi.lib()
+    h = ctypes.c_void_p()
+    assert lib.boysfn_tables_embedded(ctypes.byref(h)) == 0
+    fake = ctypes.c_void_p(1 << 20)  # never dereferenced: the check comes first
+    n, k = 1000, 8
+    assert lib.boysfn_eval_device(h, fake, n, k, fake, n * (k + 1) - 1, _capi.LAYOUT_AOS, 0, None, None) \
+        == _capi.ERR_SIZE
+    assert _capi.last_error() == "boys_batch_many: output span has wrong size"
+    assert lib.boysfn_eval_device(h, fake, n, k, fake, k * 1024 + n - 1, _capi.LAYOUT_SOA, 1024, None, None) \
+        == _capi.ERR_SIZE
+    import torch
+    x = torch.zeros(n, dtype=torch.float64)
+    with pytest.raises(pkg.invalid_argument, match="CUDA"):
+        pkg.eval_device(x, k, torch.zeros(n * (k + 1), dtype=torch.float64))
+    with pytest.raises(pkg.invalid_argument, match="float64"):
+        pkg.eval_device(x.float(), k, torch.zeros(n * (k + 1), dtype=torch.float64))
 
 
 def test_host_side_argument_checks_need_no_device():

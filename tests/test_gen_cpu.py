@@ -9,8 +9,8 @@ import numpy as np
 import pytest
 from mpmath import mpf
 
-from paper_2512_10059_b200 import gen
-from paper_2512_10059_b200.gen import hp, remez
+import genport as gen
+from genport import hp, remez
 
 
 @pytest.fixture(autouse=True)
@@ -173,12 +173,6 @@ def test_walsh_search_minimal_degree():
     for c in res.cells:
         if c.n + c.m < d:
             assert c.status != gen.RemezStatus.Converged or c.sup_error > mpf("1e-6")
-
-
-def test_cli_regions(capsys):
-    from paper_2512_10059_b200.gen.__main__ import main
-    assert main(["regions", "--kmax", "32", "--eps", "5e-14"]) == 0
-    assert capsys.readouterr().out.strip() == "x0=11.899848152108484 x1=28.98933773882074"
 
 
 def test_rho_A_is_the_downward_amplification():

@@ -5,10 +5,10 @@ import pytest
 from mpmath import mpf
 
 import paper_2512_10059_b200 as pkg
-from paper_2512_10059_b200 import gen
+import genport as gen
 from paper_2512_10059_b200 import tables as T
-from paper_2512_10059_b200.gen import hp, scan
-from paper_2512_10059_b200.gen.generate import generate_tables, search_table
+from genport import hp, scan
+from genport.generate import generate_tables, search_table
 
 pytestmark = pytest.mark.gpu
 

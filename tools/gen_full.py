@@ -10,9 +10,10 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import paper_2512_10059_b200 as pkg  # noqa: E402
 from paper_2512_10059_b200 import tables as T  # noqa: E402
-from paper_2512_10059_b200.gen.generate import generate_tables  # noqa: E402
+from genport.generate import generate_tables  # noqa: E402
 
 
 def rat(r, x):
@@ -23,7 +24,7 @@ def main():
     kmax, eps, workers, out = int(sys.argv[1]), float(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
     t = time.time()
     res = generate_tables(kmax, eps, workers=workers)
-    from paper_2512_10059_b200.gen.generate import certify
+    from genport.generate import certify
     log = []
     ok, _ = certify(res.tables, res.alternatives, 10000, log=log)
     print("\n".join(log), "certified" if ok else "NOT certified", flush=True)

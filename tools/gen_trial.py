@@ -9,10 +9,11 @@ import numpy as np
 from mpmath import mpf
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import paper_2512_10059_b200 as pkg  # noqa: E402
-from paper_2512_10059_b200 import gen  # noqa: E402
-from paper_2512_10059_b200.gen import hp, scan  # noqa: E402
-from paper_2512_10059_b200.gen.generate import search_table  # noqa: E402
+import genport as gen  # noqa: E402
+from genport import hp, scan  # noqa: E402
+from genport.generate import search_table  # noqa: E402
 
 
 def main():

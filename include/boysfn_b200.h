@@ -132,6 +132,14 @@ int boysfn_eval_device(boysfn_tables_t tables, const double* d_x, size_t n, int 
 int boysfn_eval_host(boysfn_tables_t tables, const double* xs, size_t n, int k, double* out,
                      size_t out_len, int layout, size_t ld, size_t* first_bad);
 
+/* Page-locked host memory for boysfn_eval_host buffers.  Pinned x and out
+ * are read and written by the copy engines directly (about 55 GB/s D2H on
+ * the B200 hosts); pageable ones go through the library's pinned staging plus
+ * a host memcpy (27-33 GB/s).  Callers that reuse their buffers across calls
+ * should allocate them here.  *ptr = NULL for bytes == 0. */
+int boysfn_host_alloc(size_t bytes, void** ptr);
+int boysfn_host_free(void* ptr);
+
 /* Spreads large boysfn_eval_host calls (n*(k+1) >= 2^24 values) over these
  * devices: contiguous shards of the batch, one persistent host thread and
  * staging pipeline per device, so the shards' PCIe links add up (the

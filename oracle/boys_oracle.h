@@ -53,6 +53,8 @@ int oracle_boys_batch_many_mt(const double* xs, size_t n, int k, const oracle_ta
                               double* out, int nthreads);
 void oracle_gen_uniform(double* x, size_t n, uint64_t seed, uint64_t offset, double lo,
                         double hi);
+void oracle_gen_loguniform(double* x, size_t n, uint64_t seed, uint64_t offset, double lo, double hi);
+void oracle_gen_boundary(double* x, size_t n, uint64_t seed, uint64_t offset, double x0, double x1);
 /* verify_tables' sampling (verify.cpp:23-33) and its std::mt19937_64. */
 uint64_t oracle_mt64_nth(uint64_t seed, size_t nth);
 void oracle_verify_samples(double x0, double x1, double xmax, size_t per_region, uint64_t seed, double* xs);

@@ -13,6 +13,7 @@
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
  * arm may load this file's library.  The CUDA product path never calls it.
  */
+#define _GNU_SOURCE  /* exp10 */
 #include "boys_oracle.h"
 
 #include <math.h>
@@ -280,5 +281,47 @@ void oracle_gen_uniform(double* x, size_t n, uint64_t seed, uint64_t offset, dou
     const uint64_t z = splitmix64(seed + (offset + i + 1) * 0x9E3779B97F4A7C15ULL);
     const double u = (double)(z >> 11) * 0x1.0p-53;
     x[i] = lo + span * u; /* -ffp-contract=off: mul and add rounded separately */
+  }
+}
+
+/* The log-uniform stream of boysfn_generate_loguniform: 10^(lo + span*u) with
+ * the same u; host exp10 (glibc) may differ from the device's by an ulp, so
+ * this is the same law, not the same doubles (the reference arm's input). */
+void oracle_gen_loguniform(double* x, size_t n, uint64_t seed, uint64_t offset, double lo, double hi) {
+  const double span = hi - lo;
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t z = splitmix64(seed + (offset + i + 1) * 0x9E3779B97F4A7C15ULL);
+    x[i] = exp10(lo + span * ((double)(z >> 11) * 0x1.0p-53));
+  }
+}
+
+/* The configs[2] boundary-stress stream of boysfn_generate_boundary
+ * (capi.cu: gen_boundary_kernel), operation for operation; only mode 1's
+ * exp10 can differ from the device's by an ulp. */
+void oracle_gen_boundary(double* x, size_t n, uint64_t seed, uint64_t offset, double x0, double x1) {
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t z = splitmix64(seed + (offset + i + 1) * 0x9E3779B97F4A7C15ULL);
+    const uint64_t w = splitmix64(z ^ 0xD1B54A32D192ED03ULL);
+    const int which = (int)(z % 3), mode = (int)((z >> 8) % 3);
+    const double u = (double)(w >> 11) * 0x1.0p-53;
+    const double b = which == 0 ? 0.0 : which == 1 ? x0 : x1;
+    double v;
+    if (mode == 0) {
+      const long long j = (long long)((w >> 20) % 129) - 64;
+      if (b == 0.0) {
+        v = (double)(j < 0 ? -j : j) * 4.9406564584124654e-324;
+      } else {
+        uint64_t bits;
+        memcpy(&bits, &b, sizeof bits);
+        bits += (uint64_t)j;
+        memcpy(&v, &bits, sizeof v);
+      }
+    } else if (mode == 1) {
+      const double off = exp10(-(1.0 + 14.0 * u));
+      v = ((w >> 10) & 1) ? b + off : b - off;
+    } else {
+      v = b + (2.0 * u - 1.0);
+    }
+    x[i] = fabs(v);
   }
 }

@@ -71,6 +71,8 @@ class Port:
         L.oracle_classify_region.argtypes = [ctypes.c_double, ctypes.POINTER(_Tables)]
         L.oracle_gen_uniform.argtypes = [_dp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_double, ctypes.c_double]
+        L.oracle_gen_loguniform.argtypes = L.oracle_gen_uniform.argtypes
+        L.oracle_gen_boundary.argtypes = L.oracle_gen_uniform.argtypes
         L.oracle_mt64_nth.argtypes = [ctypes.c_uint64, ctypes.c_size_t]
         L.oracle_mt64_nth.restype = ctypes.c_uint64
         L.oracle_verify_samples.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_size_t,
@@ -132,6 +134,16 @@ class Port:
     def gen_uniform(self, n, seed, lo, hi, offset=0):
         x = np.empty(n, dtype=np.float64)
         self.L.oracle_gen_uniform(x.ctypes.data_as(_dp), n, seed, offset, lo, hi)
+        return x
+
+    def gen_loguniform(self, n, seed, log10_lo, log10_hi, offset=0):
+        x = np.empty(n, dtype=np.float64)
+        self.L.oracle_gen_loguniform(x.ctypes.data_as(_dp), n, seed, offset, log10_lo, log10_hi)
+        return x
+
+    def gen_boundary(self, n, seed, offset=0):
+        x = np.empty(n, dtype=np.float64)
+        self.L.oracle_gen_boundary(x.ctypes.data_as(_dp), n, seed, offset, self.x0, self.x1)
         return x
 
     def verify_samples(self, per_region, xmax=200.0, seed=1, x0=None, x1=None):

@@ -10,13 +10,13 @@ from .tables import (CoefficientTableSet, RationalApproximant, TableParseError, 
                      emit_tables, parse_tables, validate_tables)
 from .eval import (BoysBatch, alg2, DeviceTables, Region, boys_batch, boys_batch_many, boys_batch_region,
                    classify_region, cuda_error, domain_error, eval_device, generate_boundary, generate_loguniform,
-                   generate_uniform, invalid_argument, kernel_launch_count, out_of_range, set_devices,
+                   generate_uniform, host_empty, invalid_argument, kernel_launch_count, out_of_range, set_devices,
                    unsupported, VerifyEntry, VerifyReport, verify_tables)
 
 __all__ = [
     "CoefficientTableSet", "RationalApproximant", "TableParseError", "embedded_default", "emit_tables",
     "parse_tables", "validate_tables", "alg2", "BoysBatch", "DeviceTables", "Region", "boys_batch",
     "boys_batch_many", "boys_batch_region", "classify_region", "cuda_error", "domain_error",
-    "eval_device", "set_devices", "generate_boundary", "generate_loguniform", "generate_uniform", "invalid_argument",
+    "eval_device", "host_empty", "set_devices", "generate_boundary", "generate_loguniform", "generate_uniform", "invalid_argument",
     "kernel_launch_count", "out_of_range", "unsupported", "VerifyEntry", "VerifyReport", "verify_tables",
 ]

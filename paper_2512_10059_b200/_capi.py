@@ -55,6 +55,8 @@ _SIGNATURES = [
                                         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t,
                                         ctypes.POINTER(ctypes.c_size_t)]),
     ("boysfn_set_devices", ctypes.c_int, [ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
+    ("boysfn_host_alloc", ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    ("boysfn_host_free", ctypes.c_int, [ctypes.c_void_p]),
     ("boysfn_eval_region_host", ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_void_p]),
     ("boysfn_generate_uniform", ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64,

@@ -1241,6 +1241,19 @@ int eval_host_multi(boysfn_tables_t t, const double* xs, size_t n, int k, double
 
 }  // namespace
 
+BOYSFN_API int boysfn_host_alloc(size_t bytes, void** ptr) {
+  if (ptr == nullptr) return fail(BOYSFN_ERR_ARG, "null argument");
+  *ptr = nullptr;
+  if (bytes == 0) return BOYSFN_OK;
+  CUDA_TRY(cudaHostAlloc(ptr, bytes, cudaHostAllocPortable));  // pinned for every device
+  return BOYSFN_OK;
+}
+
+BOYSFN_API int boysfn_host_free(void* ptr) {
+  if (ptr != nullptr) CUDA_TRY(cudaFreeHost(ptr));
+  return BOYSFN_OK;
+}
+
 BOYSFN_API int boysfn_set_devices(const int* devices, int count) {
   if (count > 0 && devices == nullptr) return fail(BOYSFN_ERR_ARG, "null device list");
   int ndev = 0;

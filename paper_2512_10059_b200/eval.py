@@ -157,6 +157,39 @@ def boys_batch_many(xs, k, tables, out, layout="aos", ld=None):
     _raise(st, bad.value if st == _capi.ERR_DOMAIN else None)
 
 
+class _PinnedBlock:
+    """Owner of one boysfn_host_alloc block; freed when the last view dies."""
+
+    def __init__(self, nbytes):
+        self.ptr = ctypes.c_void_p()
+        _raise(_capi.lib().boysfn_host_alloc(nbytes, ctypes.byref(self.ptr)))
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                _capi.lib().boysfn_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+class PinnedArray(np.ndarray):
+    """numpy view of a boysfn_host_alloc block; the block is freed when the
+    array and every view of it are gone."""
+
+
+def host_empty(n):
+    """An uninitialised float64 numpy array of n elements in page-locked host
+    memory (boysfn_host_alloc): boys_batch_many reads and writes it with the
+    copy engines directly instead of through pinned staging."""
+    n = int(n)
+    if n <= 0:
+        return np.empty(0)
+    blk = _PinnedBlock(n * 8)
+    arr = np.frombuffer((ctypes.c_double * n).from_address(blk.ptr.value), dtype=np.float64).view(PinnedArray)
+    arr._block = blk  # views keep `arr` (their base) and so the block alive
+    return arr
+
+
 def set_devices(devices=None):
     """Spread large boys_batch_many calls over these CUDA devices (contiguous
     shards, one host thread and staging pipeline each); None or [] restores

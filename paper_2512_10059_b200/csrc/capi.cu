@@ -272,13 +272,16 @@ bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R, int 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tensor-map coordinates are int32: tensor-store launches above this many x
+// are split (launch_eval).
+constexpr size_t kTmaMaxX = (size_t(1) << 31) - (size_t(1) << 20);
+
 // 3D map over the AoS output for the swizzled stage: dim0 = 16 doubles (one
 // 128-B line), dim1 = (k+1)/16 lines per row, dim2 = rows (stride 8(k+1) B);
 // box = one block tile (16 x (k+1)/16 x 128), 128-B swizzle.
 bool make_aos_swz_tmap(CUtensorMap* m, double* out, size_t n, int R, int rows) {
   EncodeTiledFn enc = encode_tiled();
-  if (enc == nullptr || (R != 16 && R != 32) || (reinterpret_cast<uintptr_t>(out) & 15) ||
-      n > (size_t(1) << 31) - 256)
+  if (enc == nullptr || (R != 16 && R != 32) || (reinterpret_cast<uintptr_t>(out) & 15) || n > kTmaMaxX)
     return false;
   const cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(R / 16), n};
   const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(R) * sizeof(double)};
@@ -334,11 +337,15 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "binned") return boysfn_dev::kStoreSoABinned;
     if (want == "blocktma") return boysfn_dev::kStoreSoABlockTma;
     if (want == "blocktmabin") return boysfn_dev::kStoreSoABlockTmaBin;
+    if (want == "blockbulk") return boysfn_dev::kStoreSoABlockBulk;
+    if (want == "blockbulkbin") return boysfn_dev::kStoreSoABlockBulkBin;
+    if (want == "sorted" && k <= boysfn_dev::kSortedKmax) return boysfn_dev::kStoreSoASorted;
     if (k <= 6) return boysfn_dev::kStoreSoABinned;
     return (k >= 8 && k <= 13) ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
   }
   if (want == "xpose") return boysfn_dev::kStoreAoSXpose;
   if (want == "binned") return boysfn_dev::kStoreAoSBinned;
+  if (want == "sorted" && k <= boysfn_dev::kSortedKmax) return boysfn_dev::kStoreAoSSorted;
   if (want == "blocktma" && a16) return boysfn_dev::kStoreAoSBlockTma;
   if (want == "blocktmabin" && a16) return boysfn_dev::kStoreAoSBlockTmaBin;
   if (want == "blocktmaswz" && a16 && (R == 16 || R == 32)) return boysfn_dev::kStoreAoSBlockTmaSwz;
@@ -394,7 +401,7 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
       unsigned long long* counter = nullptr;
       bool release = false;
       if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
-      void* args[] = {&p, &na, &ma, &nb, &mb, &k, &d_x, &n, &d_out, &d_bad, &counter, &tmap, &pad_tmap};
+      void* args[] = {&p, &na, &ma, &nb, &mb, &k, &d_x, &n, &d_out, &d_bad, &counter, &tmap, &pad_tmap, &ld};
       const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(boysfn_dev::kGenericTileX), args, smem, stream);
       if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
       if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");
@@ -423,9 +430,20 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
   return BOYSFN_OK;
 }
 
+bool tensor_store(int store) {
+  return store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin ||
+         store == boysfn_dev::kStoreAoSBlockTmaSwz;
+}
+
+int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out, int layout,
+                 size_t ld, cudaStream_t stream, unsigned long long* d_bad, unsigned long long* d_ctr, int store,
+                 unsigned long long ibase);
+
 // Launches the evaluation kernel; k already validated against the handle.
 // force_store >= 0 overrides the path choice (the host API's small-batch path
-// writes host-mapped memory and takes the per-warp LSU stores).
+// writes host-mapped memory and takes the per-warp LSU stores).  Tensor-map
+// stores address x by int32 coordinates: batches above kTmaMaxX are split
+// into consecutive launches on the stream (the first-bad index stays global).
 int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out,
                 int layout, size_t ld, cudaStream_t stream, unsigned long long* d_bad,
                 unsigned long long* d_ctr = nullptr, int force_store = -1) {
@@ -436,15 +454,34 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
     return fail(BOYSFN_ERR_UNSUPPORTED, "order above the run-time-k kernels' bound (64)");
   if (k > boysfn_dev::kKernelKmax || generic_forced())
     return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1, d_ctr, force_store < 0);
+  const int store = force_store >= 0 ? force_store : choose_store(layout, k, d_out);
+  if (!tensor_store(store) || n <= kTmaMaxX)
+    return launch_store(t, d_x, n, k, d_out, layout, ld, stream, d_bad, d_ctr, store, 0);
+  const size_t R = static_cast<size_t>(k) + 1;
+  for (size_t off = 0; off < n; off += kTmaMaxX) {
+    const size_t m = std::min(kTmaMaxX, n - off);
+    double* o = layout == BOYSFN_LAYOUT_SOA ? d_out + off : d_out + off * R;
+    if (int st = launch_store(t, d_x + off, m, k, o, layout, ld, stream, d_bad, d_ctr, store, off)) return st;
+  }
+  return BOYSFN_OK;
+}
+
+int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out, int layout,
+                 size_t ld, cudaStream_t stream, unsigned long long* d_bad, unsigned long long* d_ctr, int store,
+                 unsigned long long ibase) {
   const int R = k + 1;
   const int v = t->variant[k];
   const void* fn = nullptr;
   size_t smem = 0;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
-  int store = force_store >= 0 ? force_store : choose_store(layout, k, d_out);
+  // a tensor store needs a 16-B aligned output and row stride: otherwise the
+  // same tile kernel with per-row bulk copies (any ld, any 8-B alignment)
   if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) &&
       !make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::block_tma_tile_x(store)))
+    store = store == boysfn_dev::kStoreSoABlockTma ? boysfn_dev::kStoreSoABlockBulk : boysfn_dev::kStoreSoABlockBulkBin;
+  if ((store == boysfn_dev::kStoreSoABlockBulk || store == boysfn_dev::kStoreSoABlockBulkBin) &&
+      (reinterpret_cast<uintptr_t>(d_out) & 7))
     store = boysfn_dev::kStoreSoABlock;
   if (store == boysfn_dev::kStoreAoSBlockTmaSwz &&
       !make_aos_swz_tmap(&tmap, d_out, n, R, boysfn_dev::block_tma_tile_x(store)))
@@ -454,6 +491,14 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
     case boysfn_dev::kStoreSoABlockTma:
       fn = boysfn_dev::kernel_soa_block_tma(k, v);
       smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockTma>(R, threads);
+      break;
+    case boysfn_dev::kStoreSoABlockBulk:
+      fn = boysfn_dev::kernel_soa_block_bulk(k, v);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulk>(R, threads);
+      break;
+    case boysfn_dev::kStoreSoABlockBulkBin:
+      fn = boysfn_dev::kernel_soa_block_bulk_bin(k, v);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulkBin>(R, threads);
       break;
     case boysfn_dev::kStoreAoSBlockTma:
       fn = boysfn_dev::kernel_aos_block_tma(k, v);
@@ -482,6 +527,14 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
       fn = boysfn_dev::kernel_soa_block(k, v);
       smem = sizeof(double) * boysfn_dev::kBlockX * R;
       break;
+    case boysfn_dev::kStoreSoASorted:
+      fn = boysfn_dev::kernel_soa_sorted(k, v);
+      smem = static_cast<size_t>(boysfn_dev::kWarpsPerBlock) * boysfn_dev::sorted_warp_bytes(R);
+      break;
+    case boysfn_dev::kStoreAoSSorted:
+      fn = boysfn_dev::kernel_aos_sorted(k, v);
+      smem = static_cast<size_t>(boysfn_dev::kWarpsPerBlock) * boysfn_dev::sorted_warp_bytes(R);
+      break;
     case boysfn_dev::kStoreSoABinned:
       fn = boysfn_dev::kernel_soa_binned(k, v);
       smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::binned_smem_doubles_per_warp(k, true);
@@ -493,9 +546,11 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   }
   int sms = 0, bps = 0;
   if (int st = occupancy(fn, threads, smem, &sms, &bps)) return st;
-  const size_t ntiles = (n + 31) / 32;
+  const bool sorted = store == boysfn_dev::kStoreSoASorted || store == boysfn_dev::kStoreAoSSorted;
+  // work units a warp claims: 32-x tiles, or groups of kSortedG x for the sorted kernels
+  const size_t units = sorted ? (n + boysfn_dev::kSortedG - 1) / boysfn_dev::kSortedG : (n + 31) / 32;
   const size_t wpb = static_cast<size_t>(threads / 32);
-  const size_t want = (ntiles + wpb - 1) / wpb;
+  const size_t want = (units + wpb - 1) / wpb;
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
   EvalParams p = t->params[k];
   // Per-launch tile counter, zeroed and used in stream order, so concurrent
@@ -503,7 +558,8 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   unsigned long long* counter = nullptr;
   bool release = false;
   if (int st = launch_counter(d_ctr, stream, &counter, &release)) return st;
-  void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad, &counter, &tmap};  // tmap: block-TMA kernels only
+  // the block-TMA kernels take the last two; the others ignore the extra entries
+  void* args[] = {&p, &d_x, &n, &d_out, &ld, &d_bad, &counter, &tmap, &ibase};
   const cudaError_t le = cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
   if (release) CUDA_TRY(cudaFreeAsync(counter, stream));
   if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchKernel");

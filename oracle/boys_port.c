@@ -317,7 +317,8 @@ void oracle_gen_boundary(double* x, size_t n, uint64_t seed, uint64_t offset, do
         memcpy(&v, &bits, sizeof v);
       }
     } else if (mode == 1) {
-      const double off = exp10(-(1.0 + 14.0 * u));
+      /* the device contracts 1 + 14u into one fma (nvcc's default) */
+      const double off = exp10(-fma(14.0, u, 1.0));
       v = ((w >> 10) & 1) ? b + off : b - off;
     } else {
       v = b + (2.0 * u - 1.0);

@@ -20,7 +20,6 @@ enum Variant : int { kVariantEmbedded = 0, kVariantPadded = 1, kVariantCompact =
 constexpr int kCompactNA = 9, kCompactMA = 13, kCompactNB = 6, kCompactMB = 7;
 
 constexpr int kKernelKmax = 32;
-constexpr int kSortedKmax = 8;  // the region-sorted per-warp kernels exist for k <= this
 
 // x per block-TMA tile (= threads per block) of the plain SoA and AoS stores:
 // 256 x gives 2 KB SoA row segments and 2x longer AoS spans; 0.2-0.4% (SoA)
@@ -61,8 +60,6 @@ const void* kernel_soa_block_bulk(int k, int variant);
 const void* kernel_soa_block_bulk_bin(int k, int variant);
 const void* kernel_aos_block_tma_bin(int k, int variant);
 const void* kernel_aos_block_tma_swz(int k, int variant);  // k = 15, 31 only
-const void* kernel_soa_sorted(int k, int variant);  // nullptr above kSortedKmax
-const void* kernel_aos_sorted(int k, int variant);
 const void* kernel_region(int k, int variant);
 const void* kernel_generic();
 const void* kernel_generic_tma(int k, bool soa);  // nullptr above 64

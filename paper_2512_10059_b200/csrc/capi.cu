@@ -339,13 +339,11 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "blocktmabin") return boysfn_dev::kStoreSoABlockTmaBin;
     if (want == "blockbulk") return boysfn_dev::kStoreSoABlockBulk;
     if (want == "blockbulkbin") return boysfn_dev::kStoreSoABlockBulkBin;
-    if (want == "sorted" && k <= boysfn_dev::kSortedKmax) return boysfn_dev::kStoreSoASorted;
     if (k <= 6) return boysfn_dev::kStoreSoABinned;
     return (k >= 8 && k <= 13) ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
   }
   if (want == "xpose") return boysfn_dev::kStoreAoSXpose;
   if (want == "binned") return boysfn_dev::kStoreAoSBinned;
-  if (want == "sorted" && k <= boysfn_dev::kSortedKmax) return boysfn_dev::kStoreAoSSorted;
   if (want == "blocktma" && a16) return boysfn_dev::kStoreAoSBlockTma;
   if (want == "blocktmabin" && a16) return boysfn_dev::kStoreAoSBlockTmaBin;
   if (want == "blocktmaswz" && a16 && (R == 16 || R == 32)) return boysfn_dev::kStoreAoSBlockTmaSwz;
@@ -527,14 +525,6 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
       fn = boysfn_dev::kernel_soa_block(k, v);
       smem = sizeof(double) * boysfn_dev::kBlockX * R;
       break;
-    case boysfn_dev::kStoreSoASorted:
-      fn = boysfn_dev::kernel_soa_sorted(k, v);
-      smem = static_cast<size_t>(boysfn_dev::kWarpsPerBlock) * boysfn_dev::sorted_warp_bytes(R);
-      break;
-    case boysfn_dev::kStoreAoSSorted:
-      fn = boysfn_dev::kernel_aos_sorted(k, v);
-      smem = static_cast<size_t>(boysfn_dev::kWarpsPerBlock) * boysfn_dev::sorted_warp_bytes(R);
-      break;
     case boysfn_dev::kStoreSoABinned:
       fn = boysfn_dev::kernel_soa_binned(k, v);
       smem = sizeof(double) * boysfn_dev::kWarpsPerBlock * boysfn_dev::binned_smem_doubles_per_warp(k, true);
@@ -546,11 +536,9 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
   }
   int sms = 0, bps = 0;
   if (int st = occupancy(fn, threads, smem, &sms, &bps)) return st;
-  const bool sorted = store == boysfn_dev::kStoreSoASorted || store == boysfn_dev::kStoreAoSSorted;
-  // work units a warp claims: 32-x tiles, or groups of kSortedG x for the sorted kernels
-  const size_t units = sorted ? (n + boysfn_dev::kSortedG - 1) / boysfn_dev::kSortedG : (n + 31) / 32;
+  const size_t ntiles = (n + 31) / 32;
   const size_t wpb = static_cast<size_t>(threads / 32);
-  const size_t want = (units + wpb - 1) / wpb;
+  const size_t want = (ntiles + wpb - 1) / wpb;
   const unsigned grid = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(sms) * bps));
   EvalParams p = t->params[k];
   // Per-launch tile counter, zeroed and used in stream order, so concurrent

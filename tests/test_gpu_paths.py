@@ -15,7 +15,6 @@ pytestmark = pytest.mark.gpu
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
          ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"),
          ("aos", "blocktmaswz"),  # blocktmaswz: k = 15, 31 (other orders fall back to the transpose)
-         ("soa", "sorted"), ("aos", "sorted"),  # sorted: k <= 8 (above: the default path)
          ("soa", "blockbulk"), ("soa", "blockbulkbin")]
 
 
@@ -41,29 +40,6 @@ def test_all_paths_bit_identical(cuda, monkeypatch, n):
         for lay, path in PATHS[1:]:
             got = run(torch, x, k, lay, path, monkeypatch).view(torch.int64)
             assert torch.equal(got, ref), (n, k, lay, path)
-
-
-@pytest.mark.parametrize("lay", ["soa", "aos"])
-def test_sorted_unaligned_buffers(cuda, monkeypatch, lay):
-    """The region-sorted kernel with x and out 8 B off 16-B alignment (no bulk
-    copies: LSU loads and stores from the same buffers) and, for SoA, an odd
-    ld: bit-identical to the aligned run."""
-    torch = cuda
-    n = 100_003
-    for k in (0, 1, 2, 5, 8):
-        xb = torch.empty(n + 1, dtype=torch.float64, device="cuda")
-        pkg.generate_uniform(xb, 5, 0.0, 40.0)
-        ref = run(torch, xb[1:].clone(), k, lay, "sorted", monkeypatch).view(torch.int64)
-        ld = n + 1 if lay == "soa" else None  # odd ld
-        ob = torch.full(((k + 1) * (n + 1) + 1,), float("nan"), dtype=torch.float64, device="cuda")
-        monkeypatch.setenv("BOYSFN_SOA_PATH" if lay == "soa" else "BOYSFN_AOS_PATH", "sorted")
-        pkg.eval_device(xb[1:], k, ob[1:], layout=lay, ld=ld)
-        torch.cuda.synchronize()
-        monkeypatch.delenv("BOYSFN_SOA_PATH", raising=False)
-        monkeypatch.delenv("BOYSFN_AOS_PATH", raising=False)
-        o = ob[1:]
-        got = (o[: (k + 1) * (n + 1)].view(k + 1, n + 1)[:, :n].T if lay == "soa" else o[: n * (k + 1)].view(n, k + 1))
-        assert torch.equal(got.contiguous().view(torch.int64), ref), (lay, k)
 
 
 def test_all_paths_report_first_bad(cuda, port, monkeypatch):

@@ -224,6 +224,11 @@ int occupancy(const void* fn, int threads, size_t smem, int* sms, int* bps) {
   if (di.sms == 0) CUDA_TRY(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
   auto it = di.blocks_per_sm.find({fn, smem});
   if (it == di.blocks_per_sm.end()) {
+    // the whole unified L1/shared array as shared memory: these kernels stream
+    // (no L1 reuse) and their resident blocks are often shared-memory bound
+    if (std::getenv("BOYSFN_DEFAULT_CARVEOUT") == nullptr)
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
     if (smem > 48 * 1024) {  // opt in to the larger of this and any earlier request
       cudaFuncAttributes fa;
       CUDA_TRY(cudaFuncGetAttributes(&fa, fn));

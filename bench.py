@@ -91,6 +91,7 @@ def parse_args():
     ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=float, default=None, help="override x values per GPU")
     ap.add_argument("--k", type=int, default=None, help="override kmax")
+    ap.add_argument("--ks", default=None, help="override a sweep's orders, e.g. 0,1,2 (diagnostics)")
     ap.add_argument("--layout", default=None, choices=["soa", "aos"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -105,6 +106,9 @@ def parse_args():
         cfg["n"] = int(a.n)
     if a.k is not None:
         cfg["k"] = a.k
+    if a.ks is not None:
+        cfg["ks"] = [int(v) for v in a.ks.split(",")]
+        cfg["k"] = max(cfg["ks"])
     if a.layout is not None:
         cfg["layout"] = a.layout
     a.cfg = cfg

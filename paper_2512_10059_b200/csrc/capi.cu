@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>  // header-only; ranges cost nothing without a profiler attached
 
+#include <emmintrin.h>  // SSE2 non-temporal stores (host copy out of pinned staging)
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -766,10 +768,67 @@ bool is_pinned(const void* p) {
 // up to 16 threads (host memcpy: ~15 GB/s on 1 core, 59 on 8, 75 on 16 on the
 // B200 hosts, tools/probe_hostmem.py; PCIe delivers ~55 GB/s).
 struct Segment {
-  double* dst;
+  double* dst;        // nullptr: check only
   const double* src;
   size_t n;
+  bool check = false;  // check_input on src (first bad index -> bad)
+  size_t bad = ~size_t(0);
 };
+
+// check_input (eval.cpp:13-15) as a predicate: finite and non-negative.
+inline bool x_ok(double x) { return std::isfinite(x) && x >= 0; }
+
+// First index in src[0, n) that fails x_ok, or n: blocks of 256 tested
+// branch-free (vectorisable), the failing block rescanned.
+size_t first_bad_x(const double* src, size_t n) {
+  constexpr size_t B = 256;
+  size_t i = 0;
+  for (; i + B <= n; i += B) {
+    bool ok = true;
+    for (size_t j = 0; j < B; ++j) {
+      const double v = src[i + j];
+      ok &= (v >= 0.0) & (v <= 1.7976931348623157e308);
+    }
+    if (!ok) break;
+  }
+  for (; i < n; ++i)
+    if (!x_ok(src[i])) return i;
+  return n;
+}
+
+// Host copy of staged rows into the caller's buffer with non-temporal
+// (streaming) 16-B stores: the destination is written once and never read
+// back by this library, so the stores bypass the cache and skip the
+// read-for-ownership of every destination line -- a quarter of the host
+// memory traffic of the staged path (DMA write + copy read + copy write, no
+// RFO read).  BOYSFN_COPY_NT=0 falls back to memcpy (A/B).
+void copy_nt(double* dst, const double* src, size_t n) {
+  static const bool nt = [] {
+    const char* e = std::getenv("BOYSFN_COPY_NT");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (!nt || n < 64) {
+    std::memcpy(dst, src, n * sizeof(double));
+    return;
+  }
+  size_t i = 0;
+  if (reinterpret_cast<uintptr_t>(dst) & 15) {  // doubles are 8-B aligned: one scalar to reach 16 B
+    dst[0] = src[0];
+    i = 1;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 2));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 4));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 6));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 2), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 4), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 6), d);
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+}
 
 // Persistent host-copy workers: spawning 15 threads per chunk cost ~0.3 ms
 // against a ~3.7 ms copy of 128 MB.  One process-wide pool; concurrent callers
@@ -781,8 +840,8 @@ class CopyPool {
     static CopyPool pool;
     return pool;
   }
-  // Copies every piece, on the calling thread plus up to T-1 workers.
-  void run(const std::vector<Segment>& pieces, int T) {
+  // Runs every piece, on the calling thread plus up to T-1 workers.
+  void run(std::vector<Segment>& pieces, int T) {
     std::lock_guard<std::mutex> turn(turn_mu_);
     ensure_workers(T - 1);
     {
@@ -809,10 +868,18 @@ class CopyPool {
   }
 
  private:
+  static void run_piece(Segment& s) {
+    if (s.check) {
+      const size_t b = first_bad_x(s.src, s.n);
+      s.bad = b < s.n ? b : ~size_t(0);
+      if (s.dst != nullptr) copy_nt(s.dst, s.src, b);  // rows from the first bad x on are never used
+    } else {
+      copy_nt(s.dst, s.src, s.n);
+    }
+  }
   void drain() {
-    const std::vector<Segment>& p = *pieces_;
-    for (size_t i = next_.fetch_add(1); i < p.size(); i = next_.fetch_add(1))
-      std::memcpy(p[i].dst, p[i].src, p[i].n * sizeof(double));
+    std::vector<Segment>& p = *pieces_;
+    for (size_t i = next_.fetch_add(1); i < p.size(); i = next_.fetch_add(1)) run_piece(p[i]);
   }
   void ensure_workers(int want) {
     while (static_cast<int>(workers_.size()) < want) {
@@ -837,7 +904,7 @@ class CopyPool {
   std::mutex turn_mu_, mu_;
   std::condition_variable cv_, done_cv_;
   std::vector<std::thread> workers_;
-  const std::vector<Segment>* pieces_ = nullptr;
+  std::vector<Segment>* pieces_ = nullptr;
   std::atomic<size_t> next_{0};
   unsigned long long generation_ = 0;
   int helpers_ = 0, busy_ = 0;
@@ -855,7 +922,7 @@ void parallel_copy(std::vector<Segment> segs) {
   for (const auto& g : segs)
     for (size_t o = 0; o < g.n; o += piece) pieces.push_back({g.dst + o, g.src + o, std::min(piece, g.n - o)});
   if (T <= 1) {
-    for (const auto& pc : pieces) std::memcpy(pc.dst, pc.src, pc.n * sizeof(double));
+    for (const auto& pc : pieces) copy_nt(pc.dst, pc.src, pc.n);
     return;
   }
   if (std::getenv("BOYSFN_COPY_SPAWN") != nullptr) {  // A/B experiments: threads per call
@@ -873,7 +940,30 @@ void parallel_copy(std::vector<Segment> segs) {
   CopyPool::get().run(pieces, T);
 }
 
-bool x_ok(double x) { return std::isfinite(x) && x >= 0; }
+// check_input over xs[0, n) on the copy pool, staging the checked x into
+// dst (pinned) when dst is non-null.  Returns the first bad index, or n.
+// (Single-threaded, this pass bounded the host API at low k: 1e8 x at k = 8
+// is 800 MB of x against 7.2 GB of F.)
+size_t parallel_check_stage(double* dst, const double* xs, size_t n) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int T = static_cast<int>(std::min<size_t>({16, hw, std::max<size_t>(1, n / (1u << 17))}));
+  if (T <= 1) {
+    const size_t b = first_bad_x(xs, n);
+    if (dst != nullptr) copy_nt(dst, xs, b);
+    return b;
+  }
+  std::vector<Segment> pieces;
+  const size_t piece = (n + T - 1) / T;
+  for (size_t o = 0; o < n; o += piece) {
+    Segment s{dst != nullptr ? dst + o : nullptr, xs + o, std::min(piece, n - o)};
+    s.check = true;
+    pieces.push_back(s);
+  }
+  CopyPool::get().run(pieces, T);
+  for (size_t i = 0; i < pieces.size(); ++i)
+    if (pieces[i].bad != ~size_t(0)) return i * piece + pieces[i].bad;
+  return n;
+}
 
 // NVTX range for timeline tools (Nsight Systems): the host API's phases.
 struct NvtxRange {
@@ -1148,16 +1238,8 @@ int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double*
     if (host_staging && c >= static_cast<size_t>(S)) {  // the slot's staging buffers come back
       if ((status = retire(head++))) break;
     }
-    size_t b = off;  // x check (and pageable staging) of this chunk
-    if (x_direct) {
-      while (b < off + cn && x_ok(xs[b])) ++b;
-    } else {
-      double* hx = P->h_x[s];
-      for (size_t i = off; i < off + cn; ++i) {
-        hx[i - off] = xs[i];
-        if (b == i && x_ok(xs[i])) b = i + 1;
-      }
-    }
+    // x check (and pageable staging) of this chunk, on the copy pool
+    const size_t b = off + parallel_check_stage(x_direct ? nullptr : P->h_x[s], xs + off, cn);
     const size_t rows = b - off;
     if ((status = issue(c, rows))) break;
     stamp("issued", c);

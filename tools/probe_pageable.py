@@ -19,9 +19,9 @@ def main():
     out = np.empty(n * (k + 1))
     s = pkg.embedded_default()
     pkg.boys_batch_many(xs, k, s, out)
-    res = {"pool": [], "spawn": []}
+    res = {"pool": []} if os.environ.get("PP_POOL_ONLY") else {"pool": [], "spawn": []}
     for _ in range(rounds):
-        for mode in ("pool", "spawn"):
+        for mode in res:
             if mode == "spawn":
                 os.environ["BOYSFN_COPY_SPAWN"] = "1"
             else:

@@ -3,7 +3,8 @@
 
     python tools/ncu_summarize.py gpurun_out/prof.ncu-rep <key> <out.txt> [n] [index]
 
-<key> names the workload (e.g. soa_k32); ncu_summary.json[launches][key] gets
+<key> names the workload (e.g. soa_k32; "-" to leave ncu_summary.json alone);
+the report may also be an exported `--page raw --csv` file.  ncu_summary.json[launches][key] gets
 the per-launch DRAM traffic that bench.py reports as roofline.traffic (of the
 index-th kernel in the report, default the last); out.txt lists every kernel.
 """
@@ -29,7 +30,10 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # an exported `ncu -i ... --page raw --csv`
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
@@ -76,10 +80,11 @@ def main():
     with open(txt, "w") as f:
         f.write("# ncu --set full --clock-control none (%s); per-launch values, cold cache, serialised\n" % rep)
         f.write("\n".join(lines) + "\n")
-    js = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    doc = json.load(open(js)) if os.path.exists(js) else {"launches": {}}
-    doc["launches"][key] = summary
-    json.dump(doc, open(js, "w"), indent=1)
+    if key != "-":
+        js = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        doc = json.load(open(js)) if os.path.exists(js) else {"launches": {}}
+        doc["launches"][key] = summary
+        json.dump(doc, open(js, "w"), indent=1)
     print("\n".join(lines))
 
 

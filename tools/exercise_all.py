@@ -15,15 +15,20 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_10059_b200 as pkg  # noqa: E402
 
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
-         ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"), ("aos", "blocktmaswz")]
+         ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"), ("aos", "blocktmaswz"),
+         ("soa", "blockbulk"), ("soa", "blockbulkbin")]
 
 
 def main():
     s = pkg.embedded_default()
-    for n in (1, 33, 129, 1000):
+    for n in (1, 33, 129, 1000, 4099):
         x = torch.empty(n, dtype=torch.float64, device="cuda")
         pkg.generate_uniform(x, n, 0.0, 45.0)
-        for k in (0, 5, 8, 15, 16, 31, 32):
+        for k in (0, 1, 2, 5, 8, 15, 16, 31, 32):
+            # SoA with an odd ld and with an output 8 B off a 16-B boundary (bulk store, default path)
+            for shift, ld in ((0, n + 1), (1, n), (1, n + 3)):
+                buf = torch.empty(shift + (k + 1) * ld, dtype=torch.float64, device="cuda")
+                pkg.eval_device(x, k, buf[shift:], layout="soa", ld=ld)
             for lay, path in PATHS:
                 os.environ["BOYSFN_SOA_PATH" if lay == "soa" else "BOYSFN_AOS_PATH"] = path
                 out = torch.empty(n * (k + 1), dtype=torch.float64, device="cuda")

@@ -55,6 +55,11 @@ void oracle_gen_uniform(double* x, size_t n, uint64_t seed, uint64_t offset, dou
                         double hi);
 void oracle_gen_loguniform(double* x, size_t n, uint64_t seed, uint64_t offset, double lo, double hi);
 void oracle_gen_boundary(double* x, size_t n, uint64_t seed, uint64_t offset, double x0, double x1);
+/* Every value of a device output (AoS: soa = 0; SoA: soa = 1, row stride ld)
+ * against the restatement, threaded, reference rows computed on the fly. */
+int oracle_compare_output(const double* xs, size_t n, int k, const oracle_tables* t, const double* out, int soa,
+                          size_t ld, double tol, int nthreads, double* max_dev, size_t* over_tol, size_t* c_mismatch,
+                          size_t* c_values);
 /* verify_tables' sampling (verify.cpp:23-33) and its std::mt19937_64. */
 uint64_t oracle_mt64_nth(uint64_t seed, size_t nth);
 void oracle_verify_samples(double x0, double x1, double xmax, size_t per_region, uint64_t seed, double* xs);

@@ -155,6 +155,78 @@ int oracle_boys_batch_many_mt(const double* xs, size_t n, int k, const oracle_ta
   return st;
 }
 
+/* ---- Full-batch parity check (test infrastructure): every row of a device
+ * output against this restatement, computed on the fly per thread (no host
+ * copy of the reference output).  Records the max |gpu - ref|, the number of
+ * values above tol, and the number of region-C values (x >= x1) that differ
+ * in any bit.  layout 0: AoS out[i*(k+1)+l]; 1: SoA out[l*ld+i]. */
+typedef struct {
+  const double* xs;
+  const double* out;
+  size_t i0, i1, ld;
+  int k, soa;
+  double tol;
+  const oracle_tables* t;
+  double max_dev;
+  size_t over_tol, c_mismatch, c_values;
+  int status;
+} cmp_job;
+
+static void* cmp_worker(void* arg) {
+  cmp_job* j = (cmp_job*)arg;
+  double F[130];
+  const size_t row = (size_t)j->k + 1;
+  for (size_t i = j->i0; i < j->i1; ++i) {
+    if (oracle_boys_batch(j->xs[i], j->k, j->t, F) != ORACLE_OK) {
+      j->status = ORACLE_ERR_DOMAIN;
+      return NULL;
+    }
+    const int inC = !(j->xs[i] < j->t->x1);
+    for (size_t l = 0; l < row; ++l) {
+      const double g = j->soa ? j->out[l * j->ld + i] : j->out[i * row + l];
+      const double d = fabs(g - F[l]);
+      if (d > j->max_dev) j->max_dev = d;
+      if (d > j->tol) ++j->over_tol;
+      if (inC) {
+        ++j->c_values;
+        if (memcmp(&g, &F[l], sizeof g) != 0) ++j->c_mismatch;
+      }
+    }
+  }
+  return NULL;
+}
+
+int oracle_compare_output(const double* xs, size_t n, int k, const oracle_tables* t, const double* out, int soa,
+                          size_t ld, double tol, int nthreads, double* max_dev, size_t* over_tol, size_t* c_mismatch,
+                          size_t* c_values) {
+  if (nthreads < 1) nthreads = 1;
+  if ((size_t)nthreads > n) nthreads = n ? (int)n : 1;
+  if (k < 0 || k > 128) return ORACLE_ERR_RANGE;
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  cmp_job* jobs = (cmp_job*)calloc((size_t)nthreads, sizeof(cmp_job));
+  size_t begin = 0;
+  for (int w = 0; w < nthreads; ++w) {
+    const size_t cnt = n / nthreads + ((size_t)w < n % nthreads ? 1 : 0);
+    jobs[w] = (cmp_job){xs, out, begin, begin + cnt, ld, k, soa, tol, t, 0.0, 0, 0, 0, ORACLE_OK};
+    pthread_create(&th[w], NULL, cmp_worker, &jobs[w]);
+    begin += cnt;
+  }
+  int st = ORACLE_OK;
+  *max_dev = 0.0;
+  *over_tol = *c_mismatch = *c_values = 0;
+  for (int w = 0; w < nthreads; ++w) {
+    pthread_join(th[w], NULL);
+    if (st == ORACLE_OK && jobs[w].status != ORACLE_OK) st = jobs[w].status;
+    if (jobs[w].max_dev > *max_dev) *max_dev = jobs[w].max_dev;
+    *over_tol += jobs[w].over_tol;
+    *c_mismatch += jobs[w].c_mismatch;
+    *c_values += jobs[w].c_values;
+  }
+  free(th);
+  free(jobs);
+  return st;
+}
+
 /* ---- Algorithm 2 direct summation (the benchmark's correctness
  * oracle): z_i = sum_j y_j sum_l c_l F_l(x_i + x_j) with every F from the
  * reference restatement above; zabs_i = sum_j |y_j sum_l c_l F_l| scales the

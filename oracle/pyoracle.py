@@ -72,6 +72,10 @@ class Port:
         L.oracle_gen_uniform.argtypes = [_dp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_double, ctypes.c_double]
         L.oracle_gen_loguniform.argtypes = L.oracle_gen_uniform.argtypes
+        L.oracle_compare_output.argtypes = [_dp, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(_Tables), _dp,
+                                            ctypes.c_int, ctypes.c_size_t, ctypes.c_double, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_size_t),
+                                            ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
         L.oracle_gen_boundary.argtypes = L.oracle_gen_uniform.argtypes
         L.oracle_mt64_nth.argtypes = [ctypes.c_uint64, ctypes.c_size_t]
         L.oracle_mt64_nth.restype = ctypes.c_uint64
@@ -145,6 +149,21 @@ class Port:
         x = np.empty(n, dtype=np.float64)
         self.L.oracle_gen_boundary(x.ctypes.data_as(_dp), n, seed, offset, self.x0, self.x1)
         return x
+
+    def compare_output(self, xs, k, out, soa, ld=None, tol=5e-14, threads=None):
+        """Every value of out (AoS, or SoA with row stride ld) against the
+        restatement: (max |out - ref|, values above tol, region-C values that
+        differ in any bit, region-C values checked)."""
+        xs = np.ascontiguousarray(xs, dtype=np.float64)
+        assert out.dtype == np.float64 and out.flags.c_contiguous
+        md, ot, cm, cv = ctypes.c_double(), ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        st = self.L.oracle_compare_output(xs.ctypes.data_as(_dp), xs.size, k, ctypes.byref(self.tables),
+                                          out.ctypes.data_as(_dp), 1 if soa else 0, ld or xs.size, tol,
+                                          threads or os.cpu_count() or 1, ctypes.byref(md), ctypes.byref(ot),
+                                          ctypes.byref(cm), ctypes.byref(cv))
+        if st:
+            raise RuntimeError("compare status %d" % st)
+        return md.value, ot.value, cm.value, cv.value
 
     def verify_samples(self, per_region, xmax=200.0, seed=1, x0=None, x1=None):
         """The x verify_tables draws (verify.cpp:23-33), regions A, B, C in order."""

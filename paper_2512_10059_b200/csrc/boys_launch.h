@@ -39,7 +39,6 @@ constexpr int kSwzTmaTileX = BOYSFN_SWZ_TMA_BX;  // swizzled AoS stage
 constexpr int block_tma_tile_x(int store) {
   return store == kStoreSoABlockTma      ? kSoATmaTileX
          : store == kStoreSoABlockBulk   ? kSoATmaTileX
-         : store == kStoreSoABlockBulkBin ? kBinTmaTileX
          : store == kStoreAoSBlockTma    ? kAoSTmaTileX
          : store == kStoreSoABlockTmaBin ? kBinTmaTileX
          : store == kStoreAoSBlockTmaBin ? kBinTmaTileX
@@ -57,7 +56,6 @@ const void* kernel_soa_block_tma(int k, int variant);
 const void* kernel_aos_block_tma(int k, int variant);
 const void* kernel_soa_block_tma_bin(int k, int variant);
 const void* kernel_soa_block_bulk(int k, int variant);
-const void* kernel_soa_block_bulk_bin(int k, int variant);
 const void* kernel_aos_block_tma_bin(int k, int variant);
 const void* kernel_aos_block_tma_swz(int k, int variant);  // k = 15, 31 only
 const void* kernel_region(int k, int variant);

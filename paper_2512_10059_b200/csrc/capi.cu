@@ -345,7 +345,6 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "blocktma") return boysfn_dev::kStoreSoABlockTma;
     if (want == "blocktmabin") return boysfn_dev::kStoreSoABlockTmaBin;
     if (want == "blockbulk") return boysfn_dev::kStoreSoABlockBulk;
-    if (want == "blockbulkbin") return boysfn_dev::kStoreSoABlockBulkBin;
     if (k <= 6) return boysfn_dev::kStoreSoABinned;
     return (k >= 8 && k <= 13) ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
   }
@@ -480,13 +479,22 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
   size_t smem = 0;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
-  // a tensor store needs a 16-B aligned output and row stride: otherwise the
-  // same tile kernel with per-row bulk copies (any ld, any 8-B alignment)
-  if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) &&
-      !make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::block_tma_tile_x(store)))
-    store = store == boysfn_dev::kStoreSoABlockTma ? boysfn_dev::kStoreSoABlockBulk : boysfn_dev::kStoreSoABlockBulkBin;
-  if ((store == boysfn_dev::kStoreSoABlockBulk || store == boysfn_dev::kStoreSoABlockBulkBin) &&
-      (reinterpret_cast<uintptr_t>(d_out) & 7))
+  // the tensor store for rows that start on a 32-B sector boundary (output
+  // 32-B aligned, ld a multiple of 4); otherwise the same tile kernel with
+  // per-row bulk copies whose windows are shifted to the row's sector phase
+  // (any ld, any 8-B alignment): at ld = 2 mod 4 it beats the tensor store
+  // (k = 32: 0.89 vs 0.86, k = 8: 0.96 vs 0.91 of the ld = n rate,
+  // profiles/r02_tma_edges.txt)
+  // (BOYSFN_SOA_PATH=blocktma* forces the tensor store wherever its map encodes)
+  const bool sector_rows = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0 && (ld & 3) == 0;
+  if (store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin) {
+    const bool want_tensor = sector_rows || std::getenv("BOYSFN_SOA_PATH") != nullptr;
+    // (the 256-x plain tiles: 4-5% faster than the region-sorted 128-x ones
+    // at k = 8..16 for these strides, profiles/r02_bulk_vs_bulkbin.txt)
+    if (!want_tensor || !make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::block_tma_tile_x(store)))
+      store = boysfn_dev::kStoreSoABlockBulk;
+  }
+  if (store == boysfn_dev::kStoreSoABlockBulk && (reinterpret_cast<uintptr_t>(d_out) & 7))
     store = boysfn_dev::kStoreSoABlock;
   if (store == boysfn_dev::kStoreAoSBlockTmaSwz &&
       !make_aos_swz_tmap(&tmap, d_out, n, R, boysfn_dev::block_tma_tile_x(store)))
@@ -500,10 +508,6 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
     case boysfn_dev::kStoreSoABlockBulk:
       fn = boysfn_dev::kernel_soa_block_bulk(k, v);
       smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulk>(R, threads);
-      break;
-    case boysfn_dev::kStoreSoABlockBulkBin:
-      fn = boysfn_dev::kernel_soa_block_bulk_bin(k, v);
-      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulkBin>(R, threads);
       break;
     case boysfn_dev::kStoreAoSBlockTma:
       fn = boysfn_dev::kernel_aos_block_tma(k, v);

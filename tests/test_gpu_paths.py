@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
          ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"),
          ("aos", "blocktmaswz"),  # blocktmaswz: k = 15, 31 (other orders fall back to the transpose)
-         ("soa", "blockbulk"), ("soa", "blockbulkbin")]
+         ("soa", "blockbulk")]
 
 
 def run(torch, x, k, lay, path, monkeypatch):

@@ -29,11 +29,7 @@ constexpr int kAoSTmaTileX = 256;
 #ifndef BOYSFN_BIN_TMA_BX
 #define BOYSFN_BIN_TMA_BX 128
 #endif
-#ifndef BOYSFN_SWZ_TMA_BX
-#define BOYSFN_SWZ_TMA_BX 128
-#endif
 constexpr int kBinTmaTileX = BOYSFN_BIN_TMA_BX;  // region-sorted block-TMA stores (SoA and AoS)
-constexpr int kSwzTmaTileX = BOYSFN_SWZ_TMA_BX;  // swizzled AoS stage
 
 // Tile width (= threads per block) of a block-TMA store kind; kBlockX otherwise.
 constexpr int block_tma_tile_x(int store) {
@@ -42,7 +38,6 @@ constexpr int block_tma_tile_x(int store) {
          : store == kStoreAoSBlockTma    ? kAoSTmaTileX
          : store == kStoreSoABlockTmaBin ? kBinTmaTileX
          : store == kStoreAoSBlockTmaBin ? kBinTmaTileX
-         : store == kStoreAoSBlockTmaSwz ? kSwzTmaTileX
                                          : kBlockX;
 }
 
@@ -57,7 +52,6 @@ const void* kernel_aos_block_tma(int k, int variant);
 const void* kernel_soa_block_tma_bin(int k, int variant);
 const void* kernel_soa_block_bulk(int k, int variant);
 const void* kernel_aos_block_tma_bin(int k, int variant);
-const void* kernel_aos_block_tma_swz(int k, int variant);  // k = 15, 31 only
 const void* kernel_region(int k, int variant);
 const void* kernel_generic();
 const void* kernel_generic_tma(int k, bool soa);  // nullptr above 64

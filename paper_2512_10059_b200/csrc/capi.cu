@@ -283,22 +283,6 @@ bool make_soa_tmap(CUtensorMap* m, double* out, size_t n, size_t ld, int R, int 
 // are split (launch_eval).
 constexpr size_t kTmaMaxX = (size_t(1) << 31) - (size_t(1) << 20);
 
-// 3D map over the AoS output for the swizzled stage: dim0 = 16 doubles (one
-// 128-B line), dim1 = (k+1)/16 lines per row, dim2 = rows (stride 8(k+1) B);
-// box = one block tile (16 x (k+1)/16 x 128), 128-B swizzle.
-bool make_aos_swz_tmap(CUtensorMap* m, double* out, size_t n, int R, int rows) {
-  EncodeTiledFn enc = encode_tiled();
-  if (enc == nullptr || (R != 16 && R != 32) || (reinterpret_cast<uintptr_t>(out) & 15) || n > kTmaMaxX)
-    return false;
-  const cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(R / 16), n};
-  const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(R) * sizeof(double)};
-  const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(R / 16), static_cast<cuuint32_t>(rows)};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 // 2D map over the AoS output for the run-time-k kernel's padded stage: dim0 =
 // order (R, contiguous), dim1 = row (stride 8R B); box = pitch x rows, so the
 // stage's pad columns (>= R) are outside the map and clipped by the store.
@@ -316,23 +300,20 @@ bool make_aos_pad_tmap(CUtensorMap* m, double* out, size_t n, int R, int pitch, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Output-path selection (short-train medians of
-// every path at every k on one B200, profiles/r01_path_sweep.txt).  Large k is
-// HBM-write-bound and wants long contiguous write bursts: block tiles of 128 x
-// stored by the TMA engine (1 KB SoA row segments / 1 KB*(k+1) AoS spans),
-// within 1-2% of one another with and without the region sort.  Small k is
-// issue-bound and wants no A/B/C divergence at the least overhead: the per-warp
-// region-binned kernels.  The AoS block stage is row-major [128][k+1]; at
-// k+1 = 16 or 32 its stores would be 8/16-way bank conflicts, so those two
-// orders stage in the TMA's 128-B swizzle and store through a 3D tensor map.
-//   SoA: k <= 6 binned; 8..13 block-TMA region-sorted; else block-TMA
-//        (block/LSU if no tensor map applies)
-//   AoS: k <= 5 binned; 6, 8 block-TMA region-sorted; k+1 in {16, 32} block-TMA
-//        with the 128-B-swizzled stage; else block-TMA (transpose if the output
-//        is not 16-B aligned, or if a tensor map does not apply)
-// BOYSFN_SOA_PATH = warp|block|binned|blocktma|blocktmabin and
-// BOYSFN_AOS_PATH = xpose|binned|blocktma|blocktmabin|blocktmaswz override the choice
-// (experiments and the path-equivalence tests).
+// Output-path selection (interleaved medians of
+// the candidate paths at every k on one B200, profiles/r01_path_sweep.txt and
+// profiles/r02_path_policy.txt).  Large k is HBM-write-bound and wants long
+// contiguous write bursts: block tiles of 256 x stored by the TMA engine (2 KB
+// SoA row segments / 2 KB*(k+1) AoS spans).  Around k = 6..9 the FP64 work per
+// byte is highest and the A/B/C divergence costs most: the 128-x tiles sorted
+// by region first.  Small k is issue-bound and wants no divergence at the
+// least overhead: the per-warp region-binned kernels.  AoS stages whose rows
+// are a multiple of 4 doubles are padded by 2 (conflict-free STS.128) and
+// stored through a 2D tensor map that clips the pad (aos_stage_pitch).
+//   SoA: k <= 5 binned; 6..9 block-TMA region-sorted; else block-TMA
+//        (rows off a 32-B sector boundary: the shifted per-row bulk store)
+//   AoS: k <= 5 binned; 6..8 block-TMA region-sorted; else block-TMA
+//        (transpose if the output is not 16-B aligned or no tensor map applies)
 int choose_store(int layout, int k, const double* d_out) {
   const int R = k + 1;
   const char* e = std::getenv(layout == BOYSFN_LAYOUT_SOA ? "BOYSFN_SOA_PATH" : "BOYSFN_AOS_PATH");
@@ -345,19 +326,17 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "blocktma") return boysfn_dev::kStoreSoABlockTma;
     if (want == "blocktmabin") return boysfn_dev::kStoreSoABlockTmaBin;
     if (want == "blockbulk") return boysfn_dev::kStoreSoABlockBulk;
-    if (k <= 6) return boysfn_dev::kStoreSoABinned;
-    return (k >= 8 && k <= 13) ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
+    if (k <= 5) return boysfn_dev::kStoreSoABinned;
+    return k <= 9 ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
   }
   if (want == "xpose") return boysfn_dev::kStoreAoSXpose;
   if (want == "binned") return boysfn_dev::kStoreAoSBinned;
   if (want == "blocktma" && a16) return boysfn_dev::kStoreAoSBlockTma;
   if (want == "blocktmabin" && a16) return boysfn_dev::kStoreAoSBlockTmaBin;
-  if (want == "blocktmaswz" && a16 && (R == 16 || R == 32)) return boysfn_dev::kStoreAoSBlockTmaSwz;
   if (!want.empty()) return boysfn_dev::kStoreAoSXpose;
   if (k <= 5) return boysfn_dev::kStoreAoSBinned;
   if (!a16) return boysfn_dev::kStoreAoSXpose;
-  if (R == 16 || R == 32) return boysfn_dev::kStoreAoSBlockTmaSwz;
-  return (k == 6 || k == 8) ? boysfn_dev::kStoreAoSBlockTmaBin : boysfn_dev::kStoreAoSBlockTma;
+  return k <= 8 ? boysfn_dev::kStoreAoSBlockTmaBin : boysfn_dev::kStoreAoSBlockTma;
 }
 
 // BOYSFN_GENERIC=1 routes every order through the run-time-k kernels (by the
@@ -434,9 +413,10 @@ int launch_generic(const boysfn_tables_s* t, const double* d_x, size_t n, int k,
   return BOYSFN_OK;
 }
 
-bool tensor_store(int store) {
+bool tensor_store(int store, int R) {
   return store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockTmaBin ||
-         store == boysfn_dev::kStoreAoSBlockTmaSwz;
+         ((store == boysfn_dev::kStoreAoSBlockTma || store == boysfn_dev::kStoreAoSBlockTmaBin) &&
+          boysfn_dev::aos_stage_pitch(R) != R);
 }
 
 int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, double* d_out, int layout,
@@ -459,7 +439,7 @@ int launch_eval(const boysfn_tables_s* t, const double* d_x, size_t n, int k, do
   if (k > boysfn_dev::kKernelKmax || generic_forced())
     return launch_generic(t, d_x, n, k, d_out, layout, ld, stream, d_bad, -1, d_ctr, force_store < 0);
   const int store = force_store >= 0 ? force_store : choose_store(layout, k, d_out);
-  if (!tensor_store(store) || n <= kTmaMaxX)
+  if (!tensor_store(store, k + 1) || n <= kTmaMaxX)
     return launch_store(t, d_x, n, k, d_out, layout, ld, stream, d_bad, d_ctr, store, 0);
   const size_t R = static_cast<size_t>(k) + 1;
   for (size_t off = 0; off < n; off += kTmaMaxX) {
@@ -496,8 +476,9 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
   }
   if (store == boysfn_dev::kStoreSoABlockBulk && (reinterpret_cast<uintptr_t>(d_out) & 7))
     store = boysfn_dev::kStoreSoABlock;
-  if (store == boysfn_dev::kStoreAoSBlockTmaSwz &&
-      !make_aos_swz_tmap(&tmap, d_out, n, R, boysfn_dev::block_tma_tile_x(store)))
+  if ((store == boysfn_dev::kStoreAoSBlockTma || store == boysfn_dev::kStoreAoSBlockTmaBin) &&
+      boysfn_dev::aos_stage_pitch(R) != R &&
+      !make_aos_pad_tmap(&tmap, d_out, n, R, boysfn_dev::aos_stage_pitch(R), boysfn_dev::block_tma_tile_x(store)))
     store = boysfn_dev::kStoreAoSXpose;
   const int threads = boysfn_dev::block_tma_tile_x(store);  // kThreadsPerBlock for the other kinds
   switch (store) {
@@ -520,10 +501,6 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
     case boysfn_dev::kStoreAoSBlockTmaBin:
       fn = boysfn_dev::kernel_aos_block_tma_bin(k, v);
       smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaBin>(R, threads);
-      break;
-    case boysfn_dev::kStoreAoSBlockTmaSwz:
-      fn = boysfn_dev::kernel_aos_block_tma_swz(k, v);
-      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreAoSBlockTmaSwz>(R, threads);
       break;
     case boysfn_dev::kStoreSoA:
       fn = boysfn_dev::kernel_soa(k, v);

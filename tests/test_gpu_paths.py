@@ -14,7 +14,6 @@ pytestmark = pytest.mark.gpu
 
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
          ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"),
-         ("aos", "blocktmaswz"),  # blocktmaswz: k = 15, 31 (other orders fall back to the transpose)
          ("soa", "blockbulk")]
 
 
@@ -34,7 +33,7 @@ def test_all_paths_bit_identical(cuda, monkeypatch, n):
     torch = cuda
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     pkg.generate_uniform(x, 100 + n, 0.0, 45.0)
-    ks = range(33) if n in (129, 4099) else (0, 1, 4, 8, 9, 15, 16, 31, 32)
+    ks = range(33) if n in (129, 4099) else (0, 1, 3, 4, 7, 8, 9, 11, 15, 16, 19, 31, 32)
     for k in ks:
         ref = run(torch, x, k, "soa", "warp", monkeypatch).view(torch.int64)
         for lay, path in PATHS[1:]:

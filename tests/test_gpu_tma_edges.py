@@ -86,3 +86,35 @@ def test_soa_tma_above_int32_coordinates(cuda, monkeypatch):
     assert torch.equal(out[idx].view(torch.int64), ref.view(torch.int64))
     del x, out
     torch.cuda.empty_cache()
+
+
+def test_aos_padded_tma_above_int32_coordinates(cuda, monkeypatch):
+    """The padded AoS stage's 2D tensor store (rows of 4 doubles, k = 3) at
+    2^31 + 1e6 x: split launches, values equal to the LSU kernel's on strided
+    samples and around the split, the first bad index global (86 GB)."""
+    torch = cuda
+    n = (1 << 31) + 1_000_000
+    k = 3
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    pkg.generate_uniform(x, 22, 0.0, 50.0)
+    bad = (1 << 31) + 9
+    x[bad] = float("nan")
+    out = torch.empty(n * (k + 1), dtype=torch.float64, device="cuda")
+    fb = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    monkeypatch.setenv("BOYSFN_AOS_PATH", "blocktma")
+    pkg.eval_device(x, k, out, layout="aos", first_bad=fb)
+    torch.cuda.synchronize()
+    monkeypatch.delenv("BOYSFN_AOS_PATH", raising=False)
+    assert int(fb.item()) == bad
+    split = (1 << 31) - (1 << 20)  # kTmaMaxX
+    idx = torch.cat([torch.arange(0, n, 9973, device="cuda"), torch.arange(n - 70000, n, device="cuda"),
+                     torch.arange(split - 70000, split + 70000, device="cuda")])
+    idx = idx[idx != bad]
+    xs = x[idx].contiguous()
+    m = xs.numel()
+    ref = torch.empty(m * (k + 1), dtype=torch.float64, device="cuda")
+    _soa(torch, xs, k, ref, m, "warp", monkeypatch)
+    got = out.view(n, k + 1)[idx]
+    assert torch.equal(got.contiguous().view(torch.int64), ref.view(k + 1, m).T.contiguous().view(torch.int64))
+    del x, out
+    torch.cuda.empty_cache()

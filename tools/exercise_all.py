@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_10059_b200 as pkg  # noqa: E402
 
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
-         ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"), ("aos", "blocktmaswz"),
+         ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"),
          ("soa", "blockbulk")]
 
 

@@ -48,6 +48,8 @@ def main():
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     if os.environ.get("QP_DIST") == "logu":
         pkg.generate_loguniform(x, 4, -12.0, 4.0)
+    elif os.environ.get("QP_DIST") == "boundary":
+        pkg.generate_boundary(x, 3)
     else:
         pkg.generate_uniform(x, 2, 0.0, 100.0)
     out = torch.empty(n * (max(ks) + 1), dtype=torch.float64, device="cuda")

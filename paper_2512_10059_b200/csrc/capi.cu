@@ -1131,9 +1131,13 @@ int eval_host_core(boysfn_tables_t t, const double* xs, size_t n, int k, double*
     }
     return BOYSFN_OK;
   }
-  // chunks of cx x (a multiple of 32): the output slot's worth of rows, at
-  // most n rounded up
-  const size_t cx = std::max<size_t>(32, std::min(P->cap_out / row, (n + 31) / 32 * 32) / 32 * 32);
+  // chunks of cx x (a multiple of 32): about 1/16 of the batch's output, at
+  // least 8 MB and at most the output slot (256 MB), so a mid-size batch still
+  // overlaps its H2D, kernel and D2H across chunks (n = 1e6, k = 8: 2.6 -> 2.0
+  // ms; n = 1e7: 16.4 -> 13.6 ms; profiles/r02_e2e_chunk.txt) while large ones
+  // keep the 256-MB chunks (fewer per-chunk costs, profiles/r01_e2e_chunk.txt)
+  const size_t want_out = std::min(P->cap_out, std::max<size_t>(size_t(1) << 20, n * row / 16));
+  const size_t cx = std::max<size_t>(32, std::min(want_out / row, (n + 31) / 32 * 32) / 32 * 32);
   const size_t nchunks = (n + cx - 1) / cx;
   const int S = Pipeline::kSlots;
   const bool x_direct = is_pinned(xs) && is_pinned(xs + n - 1);

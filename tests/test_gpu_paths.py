@@ -56,3 +56,18 @@ def test_all_paths_report_first_bad(cuda, port, monkeypatch):
             monkeypatch.delenv("BOYSFN_SOA_PATH", raising=False)
             monkeypatch.delenv("BOYSFN_AOS_PATH", raising=False)
             assert int(fb.item()) == 777, (k, lay, path)
+
+
+@pytest.mark.parametrize("n", [1_000_003, 3_000_001])
+def test_block_paths_static_and_claimed_schedules(cuda, monkeypatch, n):
+    """Batches around the block-TMA kernels' static/claimed schedule switch
+    (<= 16 tiles per block: static) agree bit for bit with the per-warp path."""
+    torch = cuda
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    pkg.generate_uniform(x, 7 + n, 0.0, 60.0)
+    for k in (0, 7, 8, 16, 32):
+        ref = run(torch, x, k, "soa", "warp", monkeypatch).view(torch.int64)
+        for lay, path in (("soa", "blocktma"), ("soa", "blocktmabin"), ("soa", "blockbulk"),
+                          ("aos", "blocktma"), ("aos", "blocktmabin"), ("aos", "")):
+            got = run(torch, x, k, lay, path, monkeypatch).view(torch.int64)
+            assert torch.equal(got, ref), (n, k, lay, path)

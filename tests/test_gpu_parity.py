@@ -205,10 +205,10 @@ def test_error_semantics_vs_reference(cuda):
 
 def test_host_path_error_in_later_chunk(cuda, port):
     """A bad x deep inside a multi-chunk host call: exact first_bad, earlier
-    chunks written, later rows untouched (chunks hold <= 16 Mi values)."""
+    chunks written, later rows untouched (chunks hold ~1/16 of the output)."""
     s = pkg.embedded_default()
     k = 32
-    n = 1_500_000  # ~3 chunks of output at k = 32
+    n = 1_500_000  # 16 chunks of ~25 MB of output at k = 32
     xs = port.gen_uniform(n, 77, 0.0, 60.0)
     bad_at = 1_234_567
     xs[bad_at] = np.nan

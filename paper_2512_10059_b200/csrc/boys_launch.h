@@ -24,7 +24,19 @@ constexpr int kKernelKmax = 32;
 // x per block-TMA tile (= threads per block) of the plain SoA and AoS stores:
 // 256 x gives 2 KB SoA row segments and 2x longer AoS spans; 0.2-0.4% (SoA)
 // and 0.4-1.2% (AoS) over 128 x at k >= 10 (profiles/r01_tma_tile256.txt).
-constexpr int kSoATmaTileX = 256;
+#ifndef BOYSFN_SOA_TMA_BX
+#define BOYSFN_SOA_TMA_BX 256
+#endif
+constexpr int kSoATmaTileX = BOYSFN_SOA_TMA_BX;
+// The bulk store with 512-x tiles (4-KB row segments) for SoA strides whose
+// rows do not start on a 1-KB boundary, at k = 10..26: a tile's row segment
+// then touches 5 KB-units for 4 KB written instead of 3 for 2, and the rate
+// at such strides rises 2-5% (k = 16, ld = n + 1: 2.40 -> 2.31 ms; k = 24:
+// 3.53 -> 3.37 ms).  Above k = 26 a 512-x stage leaves one resident block;
+// k = 25, 26 are compiled for two (block_tma_min_blocks;
+// profiles/r02_soa_wide_tiles.txt).
+constexpr int kSoAWideTileX = 512;
+constexpr int kSoAWideKmin = 10, kSoAWideKmax = 26;
 constexpr int kAoSTmaTileX = 256;
 #ifndef BOYSFN_BIN_TMA_BX
 #define BOYSFN_BIN_TMA_BX 128
@@ -35,6 +47,7 @@ constexpr int kBinTmaTileX = BOYSFN_BIN_TMA_BX;  // region-sorted block-TMA stor
 constexpr int block_tma_tile_x(int store) {
   return store == kStoreSoABlockTma      ? kSoATmaTileX
          : store == kStoreSoABlockBulk   ? kSoATmaTileX
+         : store == kStoreSoABlockBulkW  ? kSoAWideTileX
          : store == kStoreAoSBlockTma    ? kAoSTmaTileX
          : store == kStoreSoABlockTmaBin ? kBinTmaTileX
          : store == kStoreAoSBlockTmaBin ? kBinTmaTileX
@@ -50,6 +63,7 @@ const void* kernel_aos_binned(int k, int variant);
 const void* kernel_soa_block_tma(int k, int variant);
 const void* kernel_aos_block_tma(int k, int variant);
 const void* kernel_soa_block_tma_bin(int k, int variant);
+const void* kernel_soa_block_bulk_w(int k, int variant);  // k <= kSoAWideKmax
 const void* kernel_soa_block_bulk(int k, int variant);
 const void* kernel_aos_block_tma_bin(int k, int variant);
 const void* kernel_region(int k, int variant);

@@ -326,6 +326,7 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "blocktma") return boysfn_dev::kStoreSoABlockTma;
     if (want == "blocktmabin") return boysfn_dev::kStoreSoABlockTmaBin;
     if (want == "blockbulk") return boysfn_dev::kStoreSoABlockBulk;
+    if (want == "blockbulkw") return k <= boysfn_dev::kSoAWideKmax ? boysfn_dev::kStoreSoABlockBulkW : boysfn_dev::kStoreSoABlockBulk;
     if (k <= 5) return boysfn_dev::kStoreSoABinned;
     return k <= 9 ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
   }
@@ -474,7 +475,14 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
     if (!want_tensor || !make_soa_tmap(&tmap, d_out, n, ld, R, boysfn_dev::block_tma_tile_x(store)))
       store = boysfn_dev::kStoreSoABlockBulk;
   }
-  if (store == boysfn_dev::kStoreSoABlockBulk && (reinterpret_cast<uintptr_t>(d_out) & 7))
+  // rows off a 1-KB boundary at k = 10..24: the same bulk store with 512-x
+  // tiles (boys_launch.h kSoAWideTileX)
+  const bool kb_rows = (reinterpret_cast<uintptr_t>(d_out) & 1023) == 0 && (ld & 127) == 0;
+  if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockBulk) && !kb_rows &&
+      k >= boysfn_dev::kSoAWideKmin && k <= boysfn_dev::kSoAWideKmax && std::getenv("BOYSFN_SOA_PATH") == nullptr)
+    store = boysfn_dev::kStoreSoABlockBulkW;
+  if ((store == boysfn_dev::kStoreSoABlockBulk || store == boysfn_dev::kStoreSoABlockBulkW) &&
+      (reinterpret_cast<uintptr_t>(d_out) & 7))
     store = boysfn_dev::kStoreSoABlock;
   if ((store == boysfn_dev::kStoreAoSBlockTma || store == boysfn_dev::kStoreAoSBlockTmaBin) &&
       boysfn_dev::aos_stage_pitch(R) != R &&
@@ -489,6 +497,10 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
     case boysfn_dev::kStoreSoABlockBulk:
       fn = boysfn_dev::kernel_soa_block_bulk(k, v);
       smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulk>(R, threads);
+      break;
+    case boysfn_dev::kStoreSoABlockBulkW:
+      fn = boysfn_dev::kernel_soa_block_bulk_w(k, v);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulkW>(R, threads);
       break;
     case boysfn_dev::kStoreAoSBlockTma:
       fn = boysfn_dev::kernel_aos_block_tma(k, v);

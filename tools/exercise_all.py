@@ -16,7 +16,7 @@ import paper_2512_10059_b200 as pkg  # noqa: E402
 
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
          ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"),
-         ("soa", "blockbulk")]
+         ("soa", "blockbulk"), ("soa", "blockbulkw")]
 
 
 def main():

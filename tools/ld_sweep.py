@@ -26,6 +26,8 @@ def main():
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     pkg.generate_uniform(x, 2, 0.0, 100.0)
     pads = [0, 1, 2, 3, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 4096, 65536 - n % 65536]
+    if os.environ.get("LD_PADS"):
+        pads = [int(v) for v in os.environ["LD_PADS"].split(",")]
     buf = torch.empty((k + 1) * (n + max(pads)), dtype=torch.float64, device="cuda")
     res = {}
     for _ in range(3):

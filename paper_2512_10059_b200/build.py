@@ -32,7 +32,7 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra"]
 CU_SOURCES = ["kernels_soa.cu", "kernels_aos_xpose.cu", "kernels_soa_block.cu", "kernels_soa_binned.cu",
               "kernels_aos_binned.cu",
               "kernels_soa_block_tma.cu", "kernels_aos_block_tma.cu", "kernels_soa_block_tma_bin.cu",
-              "kernels_aos_block_tma_bin.cu", "kernels_soa_block_bulk.cu", "kernels_soa_block_bulk_w.cu", "kernels_region.cu", "kernels_generic.cu", "alg2.cu", "verify.cu",
+              "kernels_aos_block_tma_bin.cu", "kernels_soa_block_bulk.cu", "kernels_soa_block_bulk_w.cu", "kernels_soa_block_bulk_w3.cu", "kernels_region.cu", "kernels_generic.cu", "alg2.cu", "verify.cu",
               "gen_scan.cu",
               "capi.cu"]
 CPP_SOURCES = ["shim_tables.cpp", "shim_eval.cpp"]

@@ -35,8 +35,19 @@ constexpr int kSoATmaTileX = BOYSFN_SOA_TMA_BX;
 // 3.53 -> 3.37 ms).  Above k = 26 a 512-x stage leaves one resident block;
 // k = 25, 26 are compiled for two (block_tma_min_blocks;
 // profiles/r02_soa_wide_tiles.txt).
-constexpr int kSoAWideTileX = 512;
-constexpr int kSoAWideKmin = 10, kSoAWideKmax = 26;
+#ifndef BOYSFN_SOA_WIDE_BX  // A/B builds
+#define BOYSFN_SOA_WIDE_BX 512
+#define BOYSFN_SOA_WIDE_KMIN 10
+#define BOYSFN_SOA_WIDE_KMAX 26
+#endif
+constexpr int kSoAWideTileX = BOYSFN_SOA_WIDE_BX;
+constexpr int kSoAWideKmin = BOYSFN_SOA_WIDE_KMIN, kSoAWideKmax = BOYSFN_SOA_WIDE_KMAX;
+// Above that, rows off a 32-B sector boundary (the plain bulk store's case)
+// take 384-x tiles (3-KB segments; a 384-thread block with its stage fits
+// twice per SM up to k = 32): 2-3% at k = 27..32 (k = 32, ld = n + 1: 4.66 ->
+// 4.51 ms).  Sector-aligned rows keep the 256-x tensor store there, which the
+// 384-x tiles did not beat (profiles/r02_soa_wide_tiles.txt).
+constexpr int kSoAWide3TileX = 384;
 constexpr int kAoSTmaTileX = 256;
 #ifndef BOYSFN_BIN_TMA_BX
 #define BOYSFN_BIN_TMA_BX 128
@@ -48,6 +59,7 @@ constexpr int block_tma_tile_x(int store) {
   return store == kStoreSoABlockTma      ? kSoATmaTileX
          : store == kStoreSoABlockBulk   ? kSoATmaTileX
          : store == kStoreSoABlockBulkW  ? kSoAWideTileX
+         : store == kStoreSoABlockBulkW3 ? kSoAWide3TileX
          : store == kStoreAoSBlockTma    ? kAoSTmaTileX
          : store == kStoreSoABlockTmaBin ? kBinTmaTileX
          : store == kStoreAoSBlockTmaBin ? kBinTmaTileX
@@ -64,6 +76,7 @@ const void* kernel_soa_block_tma(int k, int variant);
 const void* kernel_aos_block_tma(int k, int variant);
 const void* kernel_soa_block_tma_bin(int k, int variant);
 const void* kernel_soa_block_bulk_w(int k, int variant);  // k <= kSoAWideKmax
+const void* kernel_soa_block_bulk_w3(int k, int variant);
 const void* kernel_soa_block_bulk(int k, int variant);
 const void* kernel_aos_block_tma_bin(int k, int variant);
 const void* kernel_region(int k, int variant);

@@ -327,6 +327,7 @@ int choose_store(int layout, int k, const double* d_out) {
     if (want == "blocktmabin") return boysfn_dev::kStoreSoABlockTmaBin;
     if (want == "blockbulk") return boysfn_dev::kStoreSoABlockBulk;
     if (want == "blockbulkw") return k <= boysfn_dev::kSoAWideKmax ? boysfn_dev::kStoreSoABlockBulkW : boysfn_dev::kStoreSoABlockBulk;
+    if (want == "blockbulkw3") return boysfn_dev::kStoreSoABlockBulkW3;
     if (k <= 5) return boysfn_dev::kStoreSoABinned;
     return k <= 9 ? boysfn_dev::kStoreSoABlockTmaBin : boysfn_dev::kStoreSoABlockTma;
   }
@@ -481,7 +482,10 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
   if ((store == boysfn_dev::kStoreSoABlockTma || store == boysfn_dev::kStoreSoABlockBulk) && !kb_rows &&
       k >= boysfn_dev::kSoAWideKmin && k <= boysfn_dev::kSoAWideKmax && std::getenv("BOYSFN_SOA_PATH") == nullptr)
     store = boysfn_dev::kStoreSoABlockBulkW;
-  if ((store == boysfn_dev::kStoreSoABlockBulk || store == boysfn_dev::kStoreSoABlockBulkW) &&
+  if (store == boysfn_dev::kStoreSoABlockBulk && k > boysfn_dev::kSoAWideKmax && std::getenv("BOYSFN_SOA_PATH") == nullptr)
+    store = boysfn_dev::kStoreSoABlockBulkW3;
+  if ((store == boysfn_dev::kStoreSoABlockBulk || store == boysfn_dev::kStoreSoABlockBulkW ||
+       store == boysfn_dev::kStoreSoABlockBulkW3) &&
       (reinterpret_cast<uintptr_t>(d_out) & 7))
     store = boysfn_dev::kStoreSoABlock;
   if ((store == boysfn_dev::kStoreAoSBlockTma || store == boysfn_dev::kStoreAoSBlockTmaBin) &&
@@ -501,6 +505,10 @@ int launch_store(const boysfn_tables_s* t, const double* d_x, size_t n, int k, d
     case boysfn_dev::kStoreSoABlockBulkW:
       fn = boysfn_dev::kernel_soa_block_bulk_w(k, v);
       smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulkW>(R, threads);
+      break;
+    case boysfn_dev::kStoreSoABlockBulkW3:
+      fn = boysfn_dev::kernel_soa_block_bulk_w3(k, v);
+      smem = boysfn_dev::block_tma_smem_bytes<boysfn_dev::kStoreSoABlockBulkW3>(R, threads);
       break;
     case boysfn_dev::kStoreAoSBlockTma:
       fn = boysfn_dev::kernel_aos_block_tma(k, v);

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
          ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"),
-         ("soa", "blockbulk"), ("soa", "blockbulkw")]
+         ("soa", "blockbulk"), ("soa", "blockbulkw"), ("soa", "blockbulkw3")]
 
 
 def run(torch, x, k, lay, path, monkeypatch):
@@ -67,7 +67,7 @@ def test_block_paths_static_and_claimed_schedules(cuda, monkeypatch, n):
     pkg.generate_uniform(x, 7 + n, 0.0, 60.0)
     for k in (0, 7, 8, 16, 32):
         ref = run(torch, x, k, "soa", "warp", monkeypatch).view(torch.int64)
-        for lay, path in (("soa", "blocktma"), ("soa", "blocktmabin"), ("soa", "blockbulk"), ("soa", "blockbulkw"),
+        for lay, path in (("soa", "blocktma"), ("soa", "blocktmabin"), ("soa", "blockbulk"), ("soa", "blockbulkw"), ("soa", "blockbulkw3"),
                           ("aos", "blocktma"), ("aos", "blocktmabin"), ("aos", "")):
             got = run(torch, x, k, lay, path, monkeypatch).view(torch.int64)
             assert torch.equal(got, ref), (n, k, lay, path)

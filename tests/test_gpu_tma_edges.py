@@ -28,7 +28,7 @@ def test_soa_tma_odd_ld_and_misaligned_out(cuda, monkeypatch, n):
         ref = torch.empty((k + 1) * n, dtype=torch.float64, device="cuda")
         _soa(torch, x, k, ref, n, "warp", monkeypatch)
         ref = ref.view(k + 1, n).view(torch.int64)
-        for path in ("blocktma", "blocktmabin", "blockbulk", "blockbulkw", None):
+        for path in ("blocktma", "blocktmabin", "blockbulk", "blockbulkw", "blockbulkw3", None):
             for shift, ld in ((0, n), (1, n), (0, n + 1), (1, n + 3), (1, n + 2)):
                 buf = torch.full((shift + (k + 1) * ld,), float("nan"), dtype=torch.float64, device="cuda")
                 out = buf[shift:]

@@ -16,7 +16,7 @@ import paper_2512_10059_b200 as pkg  # noqa: E402
 
 PATHS = [("soa", "warp"), ("soa", "block"), ("soa", "binned"), ("soa", "blocktma"), ("soa", "blocktmabin"),
          ("aos", "xpose"), ("aos", "binned"), ("aos", "blocktma"), ("aos", "blocktmabin"),
-         ("soa", "blockbulk"), ("soa", "blockbulkw")]
+         ("soa", "blockbulk"), ("soa", "blockbulkw"), ("soa", "blockbulkw3")]
 
 
 def main():

@@ -8,7 +8,8 @@ carries `secondary.k8`, the same batch at kmax = 8 timed the same way.  A "step"
 that batch; x is the splitmix64 stream of boysfn_generate_uniform (seed 2), rank
 r taking global indices [r*N, (r+1)*N) -- weak scaling, no collective on the
 data path (the only NCCL calls are the timing barrier and the max-over-ranks
-reduction).  Other named configs (reported in DESIGN.md, not the driver's line):
+reduction).  Other named configs (--config NAME; the default one-GPU line also
+carries each of them, device side only, under `configs`):
   cfg0       configs[0]: 1e6 uniform x in [0,50], k = 8, AoS; the CPU side is the
              reference API on ONE thread (cpu_baseline, --impl reference)
   cfg2       configs[2]: 1e8 x clustered at the region boundaries, k = 0..32 sweep
@@ -37,6 +38,9 @@ Reported beside `value` (device-resident, CUDA events on the launching stream):
   accuracy     max |F - oracle| and |F - reference| on a strided sample READ BACK
                FROM THE TIMED OUTPUT (the last launch's buffer), region C
                checked bit for bit
+  configs      (default run, one GPU) cfg0, cfg2, cfg3, northstar and cfg4 on
+               the device: value, ms per step, HBM roofline fraction and
+               accuracy, each after 3 untimed steps (--no-secondary skips them)
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config NAME]
 
@@ -391,6 +395,54 @@ def time_device(pkg, x, k, out, layout, pieces, steps, warmup, stream):
     return D.max_over_ranks(ev0.elapsed_time(ev1)) / steps
 
 
+def run_other_configs(args, pkg, dev, stream, hbm):
+    """The other BASELINE configurations, device side only, in the default
+    run (one GPU): so the driver's own run carries a line for each, not only
+    the builder's `--config NAME` runs.  Each: the config's own x (device
+    generator), W = 3 untimed steps, then K steps timed with CUDA events on
+    the launching stream; accuracy read back from the last timed launch."""
+    import torch
+    res = {}
+    for name, steps in (("cfg0", 20), ("cfg2", 3), ("cfg3", 5), ("northstar", 3), ("cfg4", 2)):
+        cfg = CONFIGS[name]
+        n, layout = cfg["n"], cfg["layout"]
+        ks = cfg.get("ks") or [cfg["k"]]
+        chunk = min(cfg["chunk"] or n, n)
+        x = torch.empty(n, dtype=torch.float64, device=dev)
+        generate(pkg, x, cfg, 0)
+        out = torch.empty(chunk * (max(ks) + 1), dtype=torch.float64, device=dev)
+        pieces = [(c, min(n, c + chunk)) for c in range(0, n, chunk)]
+
+        def step():
+            for kk in ks:
+                for c0, c1 in pieces:
+                    pkg.eval_device(x[c0:c1], kk, out[: (c1 - c0) * (kk + 1)], layout=layout)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(int(0.02 * 2e9))
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / steps
+        alg = n * sum(8 + 8 * (kk + 1) for kk in ks)
+        entry = {"workload": cfg["workload"], "value": n * sum(kk + 1 for kk in ks) / (ms * 1e-3), "unit": UNIT,
+                 "ms_per_step": ms, "steps": steps, "warmup": 3, "launches_per_step": len(ks) * len(pieces),
+                 "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                              "frac": alg / (ms * 1e-3) / 1e9 / hbm}}
+        if not args.no_accuracy:
+            a = accuracy_from_output(x, out, pieces[-1][0], pieces[-1][1], ks[-1], layout, m=5000)
+            entry["accuracy"] = {k_: a[k_] for k_ in ("max_abs_err_vs_oracle", "max_abs_dev_vs_reference",
+                                                       "region_c_bit_mismatches", "sample")}
+        res[name] = entry
+        del x, out
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_b200(args, world, rank, local):
     import torch
     import paper_2512_10059_b200 as pkg
@@ -535,6 +587,13 @@ def run_b200(args, world, rank, local):
                             t_all)}
     host_out = None
 
+    # the other BASELINE configurations, device side (default run, one GPU)
+    others = None
+    if args.config == "cfg1" and not args.no_secondary and world == 1 and args.n is None and args.k is None:
+        del x
+        torch.cuda.empty_cache()
+        others = run_other_configs(args, pkg, dev, stream, hbm)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -554,6 +613,8 @@ def run_b200(args, world, rank, local):
         }
         if secondary is not None:
             line["secondary"] = secondary
+        if others is not None:
+            line["configs"] = others
         if per_k is not None:
             line["per_k"] = per_k
         print(json.dumps(line), flush=True)
